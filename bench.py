@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py -- decode-step attention latency and effective HBM GB/s of the S^2ANTA hot path
+(BASELINE.json metric) on B200.
+
+Default (N=1): BASELINE config 2 -- Llama-3.1-8B GQA decode (H=32, H_kv=8, d=128, bf16),
+32k context, batch 1, S=256 stratified, synthetic W1 (i.i.d. Gaussian) inputs.  Under
+torchrun with N ranks every rank runs its own config-2 problem with global batch id = rank
+(batch x kv-head sharding, no data-path collective -> weak scaling); NCCL is used only for
+the barrier and the max-over-ranks of the device times.
+
+Timing: W untimed warm-up steps; then K timed steps, each bracketed by CUDA events on the
+launching stream; the L2 (126 MB) is flushed by writing a 512 MiB buffer before every timed
+step, outside the events.  The whole timed loop is bracketed by barrier + synchronize.
+
+value = algorithmic bytes of all ranks / max-over-ranks mean step time, where algorithmic
+bytes = all K bytes + UNIQUE sampled V rows (union over the GQA group) + q + out
+(SURVEY sec. 8(d)).  `--impl reference` times the fp64 CPU oracle (the reference arm of
+this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decode-step attention µs and effective HBM GB/s (% of B200 peak) at 32k ctx"
+WORKLOAD = ("BASELINE config 2: Llama-3.1-8B GQA decode (32 q / 8 kv heads, d=128, bf16), 32k context, "
+            "batch 1 per GPU, S=256 stratified")
+PAPER_CONTEXT = ("paper (RTX 6000 Ada, sm_89): S2ANTA-prop S=128 1.50x and S2ANTA-flash S=2048 1.51x "
+                 "decode-kernel speedup over FlashInfer at 32k (PAPER.md:212); no absolute us published")
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+           0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1, help="sequences per GPU")
+    ap.add_argument("--seqlen", type=int, default=32768)
+    ap.add_argument("--S", type=int, default=256)
+    ap.add_argument("--mode", default="stratified", choices=["iid", "stratified", "systematic"])
+    ap.add_argument("--workload", default="gauss", choices=["gauss", "temp4", "sink"])
+    ap.add_argument("--page-size", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip dense/graph/e2e/profiled legs")
+    ap.add_argument("--seed", type=int, default=0x5A17A)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """dram bytes per launch of the score kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "score_kernel_ncu.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("dram_bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 3:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.t.join(timeout=2)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            try:
+                bits = int(r[2], 16)
+            except ValueError:
+                continue
+            for b, n in REASONS.items():
+                if bits & b and n != "gpu_idle":
+                    reasons.add(n)
+        busy = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def algorithmic_bytes(seqlens, Hkv, d, e, uniq_rows, B, H):
+    """K bytes (all keys) + unique sampled V rows + q + out."""
+    kb = sum(seqlens) * Hkv * d * e
+    vb = uniq_rows * d * e
+    return kb, vb, 2 * B * H * d * e
+
+
+def run_reference(args, rank, world):
+    """Reference arm of this tier: the fp64 CPU oracle, as it stands, on a bounded sample of
+    the workload (2 of the 8 kv-head groups of the config-2 step per timed step)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    import santa_inputs as si
+    from oracle import santa_oracle as o
+
+    if rank != 0:
+        return None
+    H, Hkv, d, n = 32, 8, 128, args.seqlen
+    inp = si.make_decode_inputs(1, H, Hkv, d, n, dtype="bf16", workload=args.workload, seed=0)
+    groups = 2
+    q = si.as_bits(inp.q)[:, :4 * groups]
+    K = si.as_bits(inp.K)[:, :groups]
+    V = si.as_bits(inp.V)[:, :groups]
+    times, uniq = [], []
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out, idx = o.santa_decode(q, K, V, [n], args.S, args.mode, args.seed, step)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            uniq.append(sum(o.unique_rows(idx[0, 4 * g:4 * g + 4]) for g in range(groups)))
+    e = 2
+    kb, vb, qo = algorithmic_bytes([n], groups, d, e, float(np.mean(uniq)), 1, 4 * groups)
+    t = float(np.mean(times))
+    cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    value = (kb + vb + qo) / t / 1e9
+    sample = f"config-2 step restricted to {groups} of 8 kv-head groups ({4 * groups} q heads), fp64 oracle"
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "us_per_step": round(t * 1e6, 1), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded torch.randn, W1 Gaussian)",
+        "config": {"workload": WORKLOAD, "sample": sample, "S": args.S, "mode": args.mode},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def cpu_baseline(inp_cpu, args, bytes_per_step):
+    """The oracle as it stands timed on this host on the full config-2 step, ~10 s budget."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+
+    import santa_inputs as si
+    from oracle import santa_oracle as o
+
+    q, K, V = si.as_bits(inp_cpu.q), si.as_bits(inp_cpu.K), si.as_bits(inp_cpu.V)
+    sl = inp_cpu.seqlens.numpy()
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < 10.0 or len(times) < 2:
+        t0 = time.perf_counter()
+        o.santa_decode(q, K, V, sl, args.S, args.mode, args.seed, len(times))
+        times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    return {"value": round(bytes_per_step / t / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "sample": f"full config-2 step (batch {inp_cpu.q.shape[0]}), {len(times)} steps in "
+                      f"{time.perf_counter() - t_start:.1f} s, median {t * 1e3:.0f} ms/step"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_01910_b200 as santa
+    import santa_inputs as si
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, H, Hkv, d, n = args.batch, 32, 8, 128, args.seqlen
+    # each rank: its own batch slice of the global job (global batch ids rank*B .. rank*B+B-1)
+    inp_cpu = si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", workload=args.workload,
+                                    seed=1000 * rank, page_size=args.page_size)
+    q = inp_cpu.q.to(dev)
+    if args.page_size:
+        K, V, pt = inp_cpu.K_pool.to(dev), inp_cpu.V_pool.to(dev), inp_cpu.page_table.to(dev)
+    else:
+        K, V, pt = inp_cpu.K.to(dev), inp_cpu.V.to(dev), None
+    seqlens = inp_cpu.seqlens.to(dev)
+    geo = santa.make_geometry(q, Hkv, n, pt, args.page_size, batch_offset=rank * B)
+    ws = santa.workspace(geo, args.S, dev)
+    out = torch.empty_like(q)
+    idx = torch.empty((B, H, args.S), dtype=torch.int32, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i, with_idx=False):
+        santa.santa_decode_attention(geo, q, K, V, seqlens, args.S, args.mode, args.seed, i, out,
+                                     idx if with_idx else None, ws, stream)
+
+    # unique V rows per step (algorithmic V bytes), measured on offsets 0..3 outside timing
+    uniq = []
+    for i in range(4):
+        step(i, True)
+        torch.cuda.synchronize()
+        ii = idx.cpu().numpy()
+        uniq.append(sum(len(np.unique(ii[b, g * (H // Hkv):(g + 1) * (H // Hkv)])) for b in range(B)
+                        for g in range(Hkv)))
+    U = float(np.mean(uniq))
+    kb, vb, qo = algorithmic_bytes([n] * B, Hkv, d, 2, U, B, H)
+    bytes_step = kb + vb + qo
+
+    for i in range(args.warmup):
+        flush.zero_()
+        step(i)
+    torch.cuda.synchronize()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev[i][0].record(stream)
+            step(args.warmup + i)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        times = [a.elapsed_time(b) for a, b in ev]  # ms
+        # keep the same workload running ~1 s so the clock sampler sees it under load
+        t_end = time.time() + 1.0
+        j = 0
+        while time.time() < t_end:
+            flush.zero_()
+            for _ in range(20):
+                step(j)
+                j += 1
+            torch.cuda.synchronize()
+    mean_ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([mean_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mean_ms = float(t.item())
+    value = world * bytes_step / (mean_ms * 1e-3) / 1e9
+
+    peak, peak_src = load_peaks()
+    res = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(mean_ms, 5), "us_per_step": round(mean_ms * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded torch.randn, W1 i.i.d. Gaussian, PAPER.md:1757-1760)",
+        "config": {"workload": WORKLOAD, "batch_per_gpu": B, "seq_len": n, "S": args.S, "mode": args.mode,
+                   "n_heads": H, "n_kv_heads": Hkv, "head_dim": d, "page_size": args.page_size or "contiguous",
+                   "inputs": args.workload, "l2": "flushed (512 MiB write) before every timed step",
+                   "parallelism": f"batch x kv-head sharding over {world} GPU(s), no data-path collective"},
+        "latency_us": {"mean": round(mean_ms * 1e3, 2), "median": round(float(np.median(times)) * 1e3, 2),
+                       "p10": round(float(np.percentile(times, 10)) * 1e3, 2),
+                       "p90": round(float(np.percentile(times, 90)) * 1e3, 2)},
+        "bytes_per_step": {"K": kb, "V_unique": vb, "q_out": qo, "unique_rows": U,
+                           "V_per_sample_convention": B * H * args.S * d * 2},
+        "pct_of_peak": {"measured_copy": round(100 * value / world / peak, 1),
+                        "spec_8TBps": round(100 * value / world / 8000.0, 1)},
+        "clocks": clk.summary(),
+        "gpu_launches": 2 * args.steps,
+        "paper_context": PAPER_CONTEXT,
+    }
+
+    if not args.no_extras:
+        # (1) dominant kernel (score pass) timed inside the step via the profiled entry point
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        sc, sg = [], []
+        for i in range(args.steps):
+            flush.zero_()
+            santa.santa_decode_attention_profiled(geo, q, K, V, seqlens, args.S, args.mode, args.seed, i, out, None,
+                                                  ws, evs, stream)
+            torch.cuda.synchronize()
+            sc.append(evs[0].elapsed_time(evs[1]))
+            sg.append(evs[1].elapsed_time(evs[2]))
+        score_ms = float(np.mean(sc))
+        achieved = (kb + B * H * d * 2) / (score_ms * 1e-3) / 1e9
+        res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                           "frac": round(achieved / peak, 4), "traffic": load_traffic(),
+                           "kernel": "score_stats_kernel<bf16,128,4> (split-KV score pass)",
+                           "peak_source": peak_src,
+                           "algorithmic_bytes_per_launch": kb + B * H * d * 2,
+                           "kernel_us": round(score_ms * 1e3, 2),
+                           "sample_gather_us": round(float(np.mean(sg)) * 1e3, 2)}
+        # (2) in-repo dense exact decode, identical protocol
+        dws = santa.workspace(geo, 1, dev)
+        dout = torch.empty_like(q)
+        dt = []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            santa.santa_dense_reference(geo, q, K, V, seqlens, dout, dws, stream)
+            b_.record(stream)
+            torch.cuda.synchronize()
+            if i >= args.warmup:
+                dt.append(a.elapsed_time(b_))
+        dms = float(np.mean(dt))
+        dbytes = 2 * kb + qo
+        res["dense_reference"] = {"us": round(dms * 1e3, 2), "GBps": round(dbytes / (dms * 1e-3) / 1e9, 1),
+                                  "santa_speedup": round(dms / mean_ms, 3)}
+        # (3) CUDA-graph replay of one step (launch overhead isolated)
+        try:
+            g = torch.cuda.CUDAGraph()
+            s2 = torch.cuda.Stream()
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s2):
+                for _ in range(2):
+                    santa.santa_decode_attention(geo, q, K, V, seqlens, args.S, args.mode, args.seed, 0, out, None,
+                                                 ws, s2)
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g):
+                santa.santa_decode_attention(geo, q, K, V, seqlens, args.S, args.mode, args.seed, 0, out, None, ws,
+                                             torch.cuda.current_stream())
+            gt = []
+            for i in range(args.steps):
+                flush.zero_()
+                a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                g.replay()
+                b_.record(stream)
+                torch.cuda.synchronize()
+                gt.append(a.elapsed_time(b_))
+            res["graph_replay_us"] = round(float(np.mean(gt)) * 1e3, 2)
+        except Exception as ex:  # graph capture is an extra, never the headline
+            res["graph_replay_us"] = f"unavailable: {type(ex).__name__}: {ex}"[:200]
+        # (4) end to end through the host-buffer C-ABI entry point
+        qh = inp_cpu.q.clone().pin_memory()
+        knh = torch.randn(B, Hkv, d).to(torch.bfloat16).pin_memory()
+        vnh = torch.randn(B, Hkv, d).to(torch.bfloat16).pin_memory()
+        outh = torch.empty_like(qh).pin_memory()
+        qd, knd, vnd, od = torch.empty_like(q), torch.empty(B, Hkv, d, dtype=torch.bfloat16, device=dev), \
+            torch.empty(B, Hkv, d, dtype=torch.bfloat16, device=dev), torch.empty_like(q)
+        et = []
+        for i in range(args.warmup + args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            santa.santa_decode_step_host(geo, qh, knh, vnh, qd, knd, vnd, K, V, seqlens, args.S, args.mode,
+                                         args.seed, i, od, outh, ws, stream)
+            t1 = time.perf_counter()
+            if i >= args.warmup:
+                et.append(t1 - t0)
+        ems = float(np.mean(et)) * 1e3
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        res["e2e"] = {"value": round(world * bytes_step / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
+                      "us_per_step": round(ems * 1e3, 2),
+                      "h2d_bytes_per_step": qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2,
+                      "d2h_bytes_per_step": outh.numel() * 2,
+                      "path": "santa_decode_step_host: pinned H2D q/k_new/v_new + KV append + decode + D2H out, "
+                              "host wall clock incl. stream sync"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        res["cpu_baseline"] = cpu_baseline(inp_cpu, args, bytes_step)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

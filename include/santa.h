@@ -1,0 +1,225 @@
+/*
+ * santa.h -- C ABI of libsanta.so: SANTA / S^2ANTA stochastic sparse decode-step
+ * attention (arXiv 2605.01910) for NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = line n of the paper text; "S:n" = SPEC.md line n;
+ * "reading #k" = the k-th interpretation of the paper listed in DESIGN.md sec. 2.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * - All tensor pointers are DEVICE pointers unless the name ends in _host.  The
+ *   caller owns every buffer; the library never allocates or frees device memory
+ *   and keeps no global mutable state (calls on different streams are reentrant).
+ * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   Calls are stream-ordered and asynchronous: a return of SANTA_OK means the
+ *   work was launched, not that it finished.
+ * - Arguments are validated synchronously on the host BEFORE anything is
+ *   launched.  On any error nothing is launched and no output is touched.  No
+ *   exception or abort crosses the ABI.  No host<->device synchronisation happens
+ *   inside any call except santa_read_error_flags and santa_decode_step_host.
+ * - Determinism: identical inputs, seed and offset give bit-identical `out` and
+ *   `idx_out` across runs (no floating-point atomics anywhere).
+ * - Device-side data errors (a seqlen < 1, i.e. an "empty distribution")
+ *   cannot be seen on the host without a sync: the kernels write zeros to that
+ *   sequence's outputs and set bit SANTA_FLAG_EMPTY_SEQ in the workspace flag
+ *   word, readable with santa_read_error_flags() after the stream is synced.
+ *
+ * Layout of the KV cache (the paper's cache is sequence-major [n_k+1, H_kv, d],
+ * P:1752; ours is head-major and optionally paged -- DESIGN.md sec. 4):
+ * - contiguous (page_table == NULL): K, V are [batch, n_kv_heads, max_seqlen, head_dim]
+ * - paged      (page_table != NULL): K, V are pools [num_pages, n_kv_heads, page_size, head_dim];
+ *   page_table is int32 [batch, max_pages_per_seq]; logical page i of sequence b is
+ *   physical page page_table[b*max_pages_per_seq + i]; token t lives in logical
+ *   page t / page_size at row t % page_size.
+ * - seqlens is a device int32 [batch]; seqlens[b] counts every cached token
+ *   INCLUDING the current one (reading #10); keys at positions >= seqlens[b]
+ *   are masked (zero mass).
+ * - q, out are [batch, n_heads, head_dim]; query head h attends kv head floor(h/G),
+ *   G = n_heads / n_kv_heads (GQA).
+ */
+#ifndef SANTA_H_
+#define SANTA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef enum {
+  SANTA_OK = 0,
+  SANTA_ERR_INVALID_ARG = 1,        /* NULL pointer, bad enum, bad scale, ...            */
+  SANTA_ERR_SHAPE = 2,              /* H % H_kv != 0, non-positive sizes, page geometry   */
+  SANTA_ERR_EMPTY_BUDGET = 3,       /* S < 1  (SPEC "empty budget") or B < 1 */
+  SANTA_ERR_EMPTY_DISTRIBUTION = 4, /* max_seqlen < 1 (SPEC "empty distribution")   */
+  SANTA_ERR_UNSUPPORTED = 5,        /* head_dim not in {64,128}, G > 8, dtype combination */
+  SANTA_ERR_WORKSPACE = 6,          /* workspace NULL, too small or not 256-B aligned     */
+  SANTA_ERR_ALIGNMENT = 7,          /* a tensor pointer not 16-byte aligned               */
+  SANTA_ERR_CUDA = 8                /* a CUDA launch/runtime call failed                  */
+} santa_status;
+
+typedef enum {
+  SANTA_IID = 0,         /* SANTA: S i.i.d. categorical draws, T_m = u_m (Eq. 4)          */
+  SANTA_STRATIFIED = 1,  /* S^2ANTA-strat: T_m = (m + u_m)/S, independent u_m                */
+  SANTA_SYSTEMATIC = 2   /* S^2ANTA-sys: T_m = (m + u_0)/S, one uniform per (b, h) (reading #2) */
+} santa_mode;
+
+typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q, K, V, out share it */
+
+#define SANTA_FLAG_EMPTY_SEQ 0x1u   /* some seqlens[b] < 1: that sequence's output was zeroed */
+
+typedef struct {
+  int32_t batch;             /* B >= 1 (sequences in this call)                                 */
+  int32_t n_heads;           /* H >= 1 query heads                                              */
+  int32_t n_kv_heads;        /* H_kv >= 1, H % H_kv == 0, G = H/H_kv <= 8                       */
+  int32_t head_dim;          /* d in {64, 128}                                                  */
+  int32_t dtype;             /* santa_dtype                                                     */
+  int32_t page_size;         /* P (tokens per page, multiple of 16) when paged; ignored otherwise */
+  int32_t max_pages_per_seq; /* columns of page_table when paged                                */
+  const int32_t* page_table; /* device int32 [batch, max_pages_per_seq] or NULL (contiguous)    */
+  int32_t max_seqlen;        /* >= every seqlens[b]; sizes the workspace and the grid           */
+  float scale;               /* score scale; 0 => 1/sqrt(head_dim) (Eq. 1)         */
+  int32_t batch_offset;      /* global batch id of row 0 (Philox keying when sharded, sec. 8(e)) */
+  int32_t head_offset;       /* global query-head id of head 0 (multiple of G when sharded)     */
+} santa_geometry;
+
+/* Human-readable name of a status code (static string, never NULL). */
+const char* santa_status_string(santa_status s);
+
+/* Library build string: version, compile target (e.g. "sm_100a") and kernel set. */
+const char* santa_version(void);
+
+/* Bytes of device workspace required by santa_decode_attention / santa_dense_reference /
+ * the seq-shard phases / santa_bernoulli_scores for this geometry and budget S
+ * (pure host arithmetic; returns 0 if the geometry is invalid).  The same workspace
+ * may be reused across calls on one stream; it must be 256-byte aligned and need not
+ * be initialised (the kernels initialise what they use). */
+size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
+
+/* SANTA / S^2ANTA decode step (the north-star hot path; Eq. 4):
+ * for every (b, h): s_j = (q_{b,h} . K_{b,kv(h),j}) * scale for j < seqlens[b]; p = softmax(s);
+ * F = CDF of p (split-KV: per-chunk max/sum + inclusive prefix, fp64 chunk combine);
+ * thresholds T_m (Philox4x32-10 stream keyed by seed, offset, global (b, h); reading #1);
+ * J_m = min{j : F(j) > T_m} (reading #4); out_{b,h} = (1/S) sum_m V_{b,kv(h),J_m}.
+ *   q [B,H,d], K/V per the layout above, seqlens [B] int32, S >= 1 (S > seqlen allowed:
+ *   sampling is with replacement), out [B,H,d] (same dtype as q),
+ *   idx_out: NULL or int32 [B,H,S] receiving J_m (token ids within the sequence).
+ * Only the LOW 32 bits of `offset` enter the Philox counter. */
+santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,
+                                    const void* V, const int32_t* seqlens, int32_t S,
+                                    int32_t mode, uint64_t seed, uint64_t offset, void* out,
+                                    int32_t* idx_out, void* workspace, size_t workspace_bytes,
+                                    void* stream);
+
+/* Same as santa_decode_attention, and additionally records three cudaEvent_t (passed as
+ * void*) on `stream`: events[0] before the score kernel, events[1] between the score
+ * kernel and the sample/gather kernel, events[2] after it.  Used by bench.py to time the
+ * dominant kernel inside the step (the events serialise the two launches). */
+santa_status santa_decode_attention_profiled(const santa_geometry* geo, const void* q,
+                                             const void* K, const void* V,
+                                             const int32_t* seqlens, int32_t S, int32_t mode,
+                                             uint64_t seed, uint64_t offset, void* out,
+                                             int32_t* idx_out, void* workspace,
+                                             size_t workspace_bytes, void* const* events,
+                                             void* stream);
+
+/* Exact dense decode attention softmax(q K^T * scale) V (Eq. 1) with the same
+ * split-KV score pass and a flash-decoding LSE combine; the in-repo reference the SANTA
+ * latency is reported against.  Arguments as above. */
+santa_status santa_dense_reference(const santa_geometry* geo, const void* q, const void* K,
+                                   const void* V, const int32_t* seqlens, void* out,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Bernoulli qK^T score stage (Eq. 5; Eq. 6; App. C), reading only
+ * the selected feature rows of a FEATURE-MAJOR key cache Kt:
+ *   contiguous Kt [B, H_kv, d, max_seqlen]; paged pool [num_pages, H_kv, d, page_size].
+ * mean_group = 1: per (b, kv-head) m_i = mean_g |q_{g,i}|, norm = max_i m_i, counts c_i of
+ *   B draws of Bernoulli(m_i/norm) (stratified: floor(B a) + 1[u < frac(B a)], reading #11;
+ *   standard: #{n : u_{i,n} < a_i}); p_hat_g = sum_{c_i>0} (norm c_i / B) q_{g,i}/m_i Kt_i.
+ * mean_group = 0: per-head ternary estimator p_hat = (norm/B) sum_i c_i sign(q_i) Kt_i.
+ * Writes scores [B, H, max_seqlen] fp32 = scale * p_hat (0 at positions >= seqlens[b]) and,
+ * if feature_mask != NULL, uint8 [B, H_kv (mean_group) or H, d] = 1 for fetched features.
+ * Philox tags 3 (mean-group, keyed by global kv-head) / 2 (per head), reading #1. */
+santa_status santa_bernoulli_scores(const santa_geometry* geo, const void* q, const void* Kt,
+                                    const int32_t* seqlens, int32_t B, int32_t stratified,
+                                    int32_t mean_group, uint64_t seed, uint64_t offset,
+                                    float* scores, uint8_t* feature_mask, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/* Config 5: Bernoulli score stage + S^2ANTA value stage: scores from
+ * santa_bernoulli_scores (kept in the workspace), then softmax -> sampling -> gather-add
+ * of V exactly as santa_decode_attention.  Bernoulli draws use (seed, offset) with tags
+ * 2/3; the value sampler uses the same (seed, offset) with tag 1. */
+santa_status santa_decode_attention_bernoulli(const santa_geometry* geo, const void* q,
+                                              const void* Kt, const void* V,
+                                              const int32_t* seqlens, int32_t B,
+                                              int32_t stratified, int32_t mean_group, int32_t S,
+                                              int32_t mode, uint64_t seed, uint64_t offset,
+                                              void* out, int32_t* idx_out, void* workspace,
+                                              size_t workspace_bytes, void* stream);
+
+/* Sequence sharding, phase 1 (config 4; reading #18).  `geo` describes THIS rank's
+ * shard: K_shard holds the shard's tokens at positions 0..shard_seqlens[b]-1.  Runs the
+ * split-KV score pass on the shard and reduces it to per-(b, h) statistics
+ *   stats_out[b,h,0] = m_r  = max_j s_j * log2(e)            (fp64; -inf if empty)
+ *   stats_out[b,h,1] = L_r  = sum_j 2^(s_j log2(e) - m_r)     (fp64; 0 if empty)
+ * stats_out is device fp64 [B, H, 2].  The per-chunk statistics and prefix stash stay in
+ * `workspace` for phase 2, which must use the same workspace. */
+santa_status santa_seqshard_stats(const santa_geometry* geo, const void* q, const void* K_shard,
+                                  const int32_t* shard_seqlens, double* stats_out,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Sequence sharding, phase 2.  stats_all is device fp64 [world, B, H, 2]: every rank's
+ * phase-1 stats (all-gathered by the caller over NCCL).  Every rank forms the identical
+ * global shard CDF F_r = sum_{r'<=r} 2^(m_r'-m*) L_r' / Z, draws the identical global
+ * thresholds T_m, keeps the strata with F_{rank-1} <= T_m < F_rank and samples them in its
+ * shard.  Writes partial_out [B, H, d] fp32 = (1/S) sum_{own m} V_{J_m} (zero if none),
+ * to be SUM-reduced across ranks by the caller, and, if idx_out != NULL, int32 [B, H, S]
+ * with the GLOBAL token id (token_offset[b] + local id) for owned strata and -1 elsewhere.
+ * token_offset: device int32 [B], this shard's first global token id per sequence. */
+santa_status santa_seqshard_sample_gather(const santa_geometry* geo, const double* stats_all,
+                                          int32_t rank, int32_t world,
+                                          const int32_t* token_offset, const void* V_shard,
+                                          const int32_t* shard_seqlens, int32_t S, int32_t mode,
+                                          uint64_t seed, uint64_t offset, float* partial_out,
+                                          int32_t* idx_out, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+
+/* End-to-end decode step through HOST buffers (used for bench.py's "e2e"): copies q_host
+ * [B,H,d] and the current token's k_new_host / v_new_host [B,H_kv,d] (pinned host memory)
+ * into the device staging buffers q_dev / k_new_dev / v_new_dev, appends k_new / v_new to
+ * the cache at position seqlens[b]-1 (the "+1 slot"), runs
+ * santa_decode_attention into out_dev and copies it to out_host; synchronises `stream`
+ * before returning.  Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
+santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_host,
+                                    const void* k_new_host, const void* v_new_host,
+                                    void* q_dev, void* k_new_dev, void* v_new_dev, void* K,
+                                    void* V, const int32_t* seqlens, int32_t S, int32_t mode,
+                                    uint64_t seed, uint64_t offset, void* out_dev,
+                                    void* out_host, void* workspace, size_t workspace_bytes,
+                                    void* stream);
+
+/* Device Philox4x32-10 uniforms for testing the device RNG against the Random123 KAT and
+ * the oracle stream: out[i] = u(draw i) of the stream (seed, offset, tag, h_global, b_global),
+ * u = r * 2^-32 (reading #1).  out is device fp64 [n]; if raw_out != NULL it receives the 4
+ * raw words of block 0 for ctr=(ctr0..3), key=(key0,key1) (KAT check). */
+santa_status santa_philox_uniforms(uint64_t seed, uint64_t offset, int32_t tag, int32_t h_global,
+                                   int32_t b_global, int32_t n, double* out, const uint32_t* ctr_key_host,
+                                   uint32_t* raw_out, void* stream);
+
+/* Reads (and clears) the workspace flag word: syncs `stream`, copies it to *flags_out. */
+santa_status santa_read_error_flags(void* workspace, uint32_t* flags_out, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SANTA_H_ */

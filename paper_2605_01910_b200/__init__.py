@@ -1,0 +1,178 @@
+"""paper_2605_01910_b200 -- B200-native SANTA / S^2ANTA stochastic sparse decode attention
+(arXiv 2605.01910).
+
+Thin Python binding over the C-ABI library ``libsanta.so`` (include/santa.h): the
+functions below have the ABI's names and only marshal torch tensors into pointers; every
+step of the hot path (scores, softmax statistics, CDF, Philox thresholds, inverse CDF,
+gather-add) runs in the sm_100a CUDA kernels.  There is no CPU fallback: importing this
+package without the built library raises ImportError, and calling it on CPU tensors
+raises ValueError.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import torch
+
+from . import _abi
+from ._abi import DTYPES, FLAG_EMPTY_SEQ, MODES, Geometry, SantaError
+
+__all__ = [
+    "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes",
+    "santa_decode_attention", "santa_decode_attention_profiled", "santa_dense_reference",
+    "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
+    "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_philox_uniforms",
+    "santa_read_error_flags", "santa_version", "decode", "dense", "LIB_PATH",
+]
+LIB_PATH = _abi.LIB_PATH
+_TORCH_DT = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float16: "f16"}
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libsanta takes CUDA tensors only (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def make_geometry(q: torch.Tensor, n_kv_heads: int, max_seqlen: int, page_table: Optional[torch.Tensor] = None,
+                  page_size: int = 0, scale: float = 0.0, batch_offset: int = 0, head_offset: int = 0) -> Geometry:
+    """Geometry struct for q [B, H, d] and a cache with n_kv_heads heads (see santa.h)."""
+    B, H, d = q.shape
+    g = Geometry()
+    g.batch, g.n_heads, g.n_kv_heads, g.head_dim = B, H, n_kv_heads, d
+    g.dtype = DTYPES[_TORCH_DT[q.dtype]]
+    g.page_table = page_table.data_ptr() if page_table is not None else None
+    g.page_size = page_size if page_table is not None else 0
+    g.max_pages_per_seq = page_table.shape[1] if page_table is not None else 0
+    g.max_seqlen = max_seqlen
+    g.scale = scale
+    g.batch_offset, g.head_offset = batch_offset, head_offset
+    return g
+
+
+def santa_version() -> str:
+    return _abi.LIB.santa_version().decode()
+
+
+def santa_workspace_bytes(geo: Geometry, S: int) -> int:
+    return int(_abi.LIB.santa_workspace_bytes(ctypes.byref(geo), S))
+
+
+def workspace(geo: Geometry, S: int, device="cuda") -> torch.Tensor:
+    n = santa_workspace_bytes(geo, S)
+    if n == 0:
+        raise SantaError("santa_workspace_bytes", 1)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def santa_decode_attention(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, stream=None):
+    _abi.check("santa_decode_attention", _abi.LIB.santa_decode_attention(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
+        _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_decode_attention_profiled(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, events,
+                                    stream=None):
+    ev = (ctypes.c_void_p * 3)(*[ctypes.c_void_p(e.cuda_event) for e in events])
+    _abi.check("santa_decode_attention_profiled", _abi.LIB.santa_decode_attention_profiled(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
+        _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), ctypes.cast(ev, ctypes.c_void_p), _stream(stream)))
+
+
+def santa_dense_reference(geo, q, K, V, seqlens, out, ws, stream=None):
+    _abi.check("santa_dense_reference", _abi.LIB.santa_dense_reference(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), _ptr(out), _ptr(ws), ws.numel(),
+        _stream(stream)))
+
+
+def santa_bernoulli_scores(geo, q, Kt, seqlens, B, stratified, mean_group, seed, offset, scores, feature_mask, ws,
+                           stream=None):
+    _abi.check("santa_bernoulli_scores", _abi.LIB.santa_bernoulli_scores(
+        ctypes.byref(geo), _ptr(q), _ptr(Kt), _ptr(seqlens), B, int(stratified), int(mean_group), seed, offset,
+        _ptr(scores), _ptr(feature_mask), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_decode_attention_bernoulli(geo, q, Kt, V, seqlens, B, stratified, mean_group, S, mode, seed, offset, out,
+                                     idx_out, ws, stream=None):
+    _abi.check("santa_decode_attention_bernoulli", _abi.LIB.santa_decode_attention_bernoulli(
+        ctypes.byref(geo), _ptr(q), _ptr(Kt), _ptr(V), _ptr(seqlens), B, int(stratified), int(mean_group), S,
+        MODES.get(mode, mode), seed, offset, _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_seqshard_stats(geo, q, K_shard, shard_seqlens, stats_out, ws, stream=None):
+    _abi.check("santa_seqshard_stats", _abi.LIB.santa_seqshard_stats(
+        ctypes.byref(geo), _ptr(q), _ptr(K_shard), _ptr(shard_seqlens), _ptr(stats_out), _ptr(ws), ws.numel(),
+        _stream(stream)))
+
+
+def santa_seqshard_sample_gather(geo, stats_all, rank, world, token_offset, V_shard, shard_seqlens, S, mode, seed,
+                                 offset, partial_out, idx_out, ws, stream=None):
+    _abi.check("santa_seqshard_sample_gather", _abi.LIB.santa_seqshard_sample_gather(
+        ctypes.byref(geo), _ptr(stats_all), rank, world, _ptr(token_offset), _ptr(V_shard), _ptr(shard_seqlens), S,
+        MODES.get(mode, mode), seed, offset, _ptr(partial_out), _ptr(idx_out), _ptr(ws), ws.numel(),
+        _stream(stream)))
+
+
+def santa_decode_step_host(geo, q_host, k_new_host, v_new_host, q_dev, k_new_dev, v_new_dev, K, V, seqlens, S, mode,
+                           seed, offset, out_dev, out_host, ws, stream=None):
+    for t in (q_host, k_new_host, v_new_host, out_host):
+        if t.is_cuda or not t.is_pinned():
+            raise ValueError("host buffers must be pinned CPU tensors")
+    hp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _abi.check("santa_decode_step_host", _abi.LIB.santa_decode_step_host(
+        ctypes.byref(geo), hp(q_host), hp(k_new_host), hp(v_new_host), _ptr(q_dev), _ptr(k_new_dev),
+        _ptr(v_new_dev), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset, _ptr(out_dev),
+        hp(out_host), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_philox_uniforms(seed, offset, tag, h_global, b_global, n, out, ctr_key: Optional[Sequence[int]] = None,
+                          raw_out=None, stream=None):
+    ck = (ctypes.c_uint32 * 6)(*ctr_key) if ctr_key is not None else None
+    _abi.check("santa_philox_uniforms", _abi.LIB.santa_philox_uniforms(
+        seed, offset, tag, h_global, b_global, n, _ptr(out), ctypes.cast(ck, ctypes.c_void_p) if ck else None,
+        _ptr(raw_out), _stream(stream)))
+
+
+def santa_read_error_flags(ws, stream=None) -> int:
+    f = ctypes.c_uint32(0)
+    _abi.check("santa_read_error_flags", _abi.LIB.santa_read_error_flags(_ptr(ws), ctypes.byref(f), _stream(stream)))
+    return int(f.value)
+
+
+# ---- convenience wrappers (allocation + the call; still no compute in Python) ----------------
+
+def decode(q, K, V, seqlens, S, mode="stratified", seed=0, offset=0, n_kv_heads=None, page_table=None,
+           page_size=0, max_seqlen=None, return_idx=False, ws=None, batch_offset=0, head_offset=0):
+    """Allocate out (+ idx) and workspace, run santa_decode_attention.  K/V are either the
+    contiguous [B, H_kv, n_max, d] cache or the paged pool [pages, H_kv, P, d]."""
+    Hkv = n_kv_heads or K.shape[1]
+    n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    geo = make_geometry(q, Hkv, n_max, page_table, page_size, batch_offset=batch_offset, head_offset=head_offset)
+    if ws is None:
+        ws = workspace(geo, S, q.device)
+    out = torch.empty_like(q)
+    idx = torch.empty((q.shape[0], q.shape[1], S), dtype=torch.int32, device=q.device) if return_idx else None
+    santa_decode_attention(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx, ws)
+    return (out, idx) if return_idx else out
+
+
+def dense(q, K, V, seqlens, n_kv_heads=None, page_table=None, page_size=0, max_seqlen=None, ws=None):
+    Hkv = n_kv_heads or K.shape[1]
+    n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    geo = make_geometry(q, Hkv, n_max, page_table, page_size)
+    if ws is None:
+        ws = workspace(geo, 1, q.device)
+    out = torch.empty_like(q)
+    santa_dense_reference(geo, q, K, V, seqlens, out, ws)
+    return out

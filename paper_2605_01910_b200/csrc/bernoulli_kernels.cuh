@@ -1,0 +1,218 @@
+// bernoulli_kernels.cuh -- Bernoulli qK^T score stage (Eq. 5
+// P:436-440, Eq. 6, App. C).  The paper implemented no kernel for it
+// (P:47); this is new.
+//
+// bern_weights_kernel (one CTA per (b, kv-head), one thread per feature i):
+//   mean-group (default): m_i = (1/G) sum_g |q_{g,i}|, norm = max_i m_i (reading #12),
+//     a_i = m_i / norm, counts c_i from Philox tag 3 keyed by the GLOBAL kv-head,
+//     stratified c_i = floor(B a_i) + 1[u_i < frac(B a_i)] (reading #11) or standard
+//     c_i = #{n < B : u_{i,n} < a_i};  w_{g,i} = ((norm c_i / B) q_{g,i}) / m_i on the
+//     selected set {c_i > 0, m_i > 0} (reading #14).
+//   per-head ternary: norm_g = max_i |q_{g,i}|, counts from tag 2 keyed by the global head,
+//     w_{g,i} = (norm_g / B) c_{g,i} sign(q_{g,i}); fetched set = union over the group (#15).
+//   Every integer decision (a_i, floor, frac, compare) is taken in fp64, as in the oracle.
+//   Output: fp32 weights [G][D], the compacted selected-feature list, the feature mask.
+// bern_chunk_kernel (one CTA per 256-key chunk of (b, kv-head)): reads ONLY the selected
+//   rows of the feature-major cache Kt, p_hat_g[k] = sum_{i in F} w_{g,i} Kt[i][k] (fp32
+//   FMA; warp w takes features w, w+4, ...; lane takes 8 consecutive keys = one 16-B load),
+//   writes scale * p_hat to `scores` if requested, then the same chunk max / exp2 / prefix
+//   epilogue as the exact score pass -> the S^2ANTA sampler runs unchanged.
+#pragma once
+#include "common.cuh"
+#include "philox.cuh"
+#include "score_kernels.cuh"
+
+namespace santa {
+
+struct BernParams {
+  const void* q;            // [B, H, D]
+  const void* Kt;           // feature-major, see KtLayout
+  const int32_t* seqlens;
+  int B, H, Hkv, nB, stratified, mean_group;
+  uint64_t seed, offset;
+  int batch_offset, head_offset;
+  float scale;              // natural-units scale for the scores output
+  float* w;                 // [B*Hkv][G][D] fp32 weights
+  int* sel;                 // [B*Hkv][D] selected features, count in sel_n
+  int* sel_n;               // [B*Hkv]
+  uint8_t* feature_mask;    // [B, Hkv or H, D] or NULL
+  // chunk kernel
+  const int32_t* page_table;
+  int page_size, max_pages;
+  float* scores;            // [B, H, score_stride] or NULL
+  int score_stride;
+  float* stash;
+  float2* cstats;
+  int Cmax, stash_stride;
+  uint32_t* tickets;
+  uint32_t* flags;
+};
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
+  __shared__ double sred[D / 32];
+  __shared__ int sCount;
+  const int kvh = blockIdx.x, b = blockIdx.y, i = threadIdx.x;
+  const size_t unit = (size_t)b * p.Hkv + kvh;
+  const T* q = reinterpret_cast<const T*>(p.q) + ((size_t)b * p.H + (size_t)kvh * G) * D;
+  if (i == 0) sCount = 0;
+  double qd[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) qd[g] = (double)Elem<T>::to_f(q[g * D + i]);
+
+  auto block_max = [&](double v) -> double {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((i & 31) == 0) sred[i >> 5] = v;
+    __syncthreads();
+    double r = sred[0];
+#pragma unroll
+    for (int k = 1; k < D / 32; ++k) r = fmax(r, sred[k]);
+    return r;
+  };
+  auto counts = [&](double a, uint32_t tag, uint32_t id) -> int {
+    PhiloxStream ps(p.seed, p.offset, tag, id, (uint32_t)(p.batch_offset + b));
+    if (p.stratified) {
+      const double Ba = (double)p.nB * a;
+      const double fl = floor(Ba);
+      return (int)fl + (ps.uniform((uint32_t)i) < (Ba - fl) ? 1 : 0);
+    }
+    int c = 0;
+    for (int n = 0; n < p.nB; ++n) c += ps.uniform((uint32_t)(i * p.nB + n)) < a ? 1 : 0;
+    return c;
+  };
+
+  float* w = p.w + unit * G * D;
+  bool selected = false;
+  if (p.mean_group) {
+    double m = 0.0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) m += fabs(qd[g]);
+    m = m / (double)G;
+    const double norm = block_max(m);
+    int c = 0;
+    if (norm > 0.0) c = counts(m / norm, kTagBernoulliGroup, (uint32_t)(p.head_offset / G + kvh));
+    selected = c > 0 && m > 0.0;
+    const double mhat = norm * (double)c / (double)p.nB;
+#pragma unroll
+    for (int g = 0; g < G; ++g) w[g * D + i] = selected ? (float)((mhat * qd[g]) / m) : 0.f;
+    if (p.feature_mask) p.feature_mask[unit * D + i] = selected ? 1 : 0;
+  } else {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const double norm = block_max(fabs(qd[g]));
+      int c = 0;
+      if (norm > 0.0) c = counts(fabs(qd[g]) / norm, kTagBernoulliHead, (uint32_t)(p.head_offset + kvh * G + g));
+      const double sg = qd[g] > 0.0 ? 1.0 : (qd[g] < 0.0 ? -1.0 : 0.0);
+      w[g * D + i] = c ? (float)((norm / (double)p.nB) * (double)c * sg) : 0.f;
+      selected |= c > 0;
+      if (p.feature_mask) p.feature_mask[((size_t)b * p.H + kvh * G + g) * D + i] = c > 0 ? 1 : 0;
+    }
+  }
+  // compact the selected features in increasing i (deterministic order)
+  __syncthreads();
+  const unsigned bal = __ballot_sync(0xffffffffu, selected);
+  __shared__ int sWarpCnt[D / 32];
+  if ((i & 31) == 0) sWarpCnt[i >> 5] = __popc(bal);
+  __syncthreads();
+  int base = 0;
+  for (int k = 0; k < (i >> 5); ++k) base += sWarpCnt[k];
+  if (selected) p.sel[unit * D + base + __popc(bal & ((1u << (i & 31)) - 1u))] = i;
+  if (i == D - 1) {
+    int tot = 0;
+    for (int k = 0; k < D / 32; ++k) tot += sWarpCnt[k];
+    p.sel_n[unit] = tot;
+  }
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams p) {
+  __shared__ __align__(16) float sS[G * kChunk];
+  __shared__ __align__(16) float sAcc[4][G][kChunk];
+  __shared__ float sW[G][D];
+  __shared__ int sSel[D];
+  pdl_wait_primary();
+  pdl_launch_dependents();
+  const int c = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+  if (c == 0 && threadIdx.x == 0) {
+    if (p.tickets) p.tickets[b * p.Hkv + kvh] = 0u;
+    if (b == 0 && kvh == 0 && p.flags) *p.flags = 0u;
+  }
+  const int seqlen = __ldg(p.seqlens + b);
+  const int chunk_start = c * kChunk;
+  const int n_valid = min(kChunk, seqlen - chunk_start);
+  const size_t unit = (size_t)b * p.Hkv + kvh;
+  const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
+  float2* cst = p.cstats + bh0 * p.Cmax + c;
+  if (n_valid <= 0) {
+    if (threadIdx.x < G) cst[(size_t)threadIdx.x * p.Cmax] = make_float2(-INFINITY, 0.f);
+    if (p.scores && chunk_start < p.score_stride)
+      for (int t = threadIdx.x; t < G * kChunk; t += kScoreThreads) {
+        const int k = chunk_start + t % kChunk;
+        if (k < p.score_stride) p.scores[(bh0 + t / kChunk) * p.score_stride + k] = 0.f;
+      }
+    return;
+  }
+  const int nsel = p.sel_n[unit];
+  for (int t = threadIdx.x; t < G * D; t += kScoreThreads) sW[t / D][t % D] = p.w[unit * G * D + t];
+  for (int t = threadIdx.x; t < nsel; t += kScoreThreads) sSel[t] = p.sel[unit * D + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = p.page_table ? p.page_size : p.score_stride;  // contiguous: page = whole row
+  const int kl = 8 * lane;            // this lane's 8 keys within the chunk
+  const int t0 = chunk_start + kl;
+  const int page = t0 / P, within = t0 - page * P;
+  const int64_t phys = p.page_table ? (int64_t)__ldg(p.page_table + (int64_t)b * p.max_pages + page) : b;
+  const T* Kt = reinterpret_cast<const T*>(p.Kt) + ((phys * p.Hkv + kvh) * D) * (int64_t)P + within;
+  float acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+  const bool live = kl < n_valid;
+  for (int s = warp; s < nsel; s += 4) {
+    const int i = sSel[s];
+    float v[8];
+    if (live) {
+      const T* src = Kt + (int64_t)i * P;
+      if constexpr (sizeof(T) == 2) {
+        const uint4 r = ldg_stream(src);
+        const uint32_t wv[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { v[2 * e] = Elem<T>::lo(wv[e]); v[2 * e + 1] = Elem<T>::hi(wv[e]); }
+      } else {
+        const uint4 r0 = ldg_stream(src), r1 = ldg_stream(src + 4);
+        v[0] = __uint_as_float(r0.x); v[1] = __uint_as_float(r0.y); v[2] = __uint_as_float(r0.z); v[3] = __uint_as_float(r0.w);
+        v[4] = __uint_as_float(r1.x); v[5] = __uint_as_float(r1.y); v[6] = __uint_as_float(r1.z); v[7] = __uint_as_float(r1.w);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float wg = sW[g][i];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(wg, v[e], acc[g][e]);
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) sAcc[warp][g][kl + e] = acc[g][e];
+  __syncthreads();
+  const float sl2 = p.scale * kLog2e;
+  for (int t = threadIdx.x; t < G * kChunk; t += kScoreThreads) {
+    const int g = t / kChunk, k = t % kChunk;
+    const float ph = ((sAcc[0][g][k] + sAcc[1][g][k]) + sAcc[2][g][k]) + sAcc[3][g][k];
+    const bool valid = k < n_valid;
+    sS[g * kChunk + k] = valid ? ph * sl2 : -INFINITY;
+    if (p.scores && chunk_start + k < p.score_stride)
+      p.scores[(bh0 + g) * p.score_stride + chunk_start + k] = valid ? ph * p.scale : 0.f;
+  }
+  __syncthreads();
+  if (p.stash) chunk_stats_prefix<G>(sS, p.stash + bh0 * p.stash_stride + chunk_start, p.stash_stride, cst, p.Cmax);
+}
+
+}  // namespace santa

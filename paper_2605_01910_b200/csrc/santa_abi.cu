@@ -1,0 +1,614 @@
+// santa_abi.cu -- host side of libsanta.so: argument validation, workspace layout,
+// template dispatch and (PDL-chained) launches.  See include/santa.h for the contract.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "bernoulli_kernels.cuh"
+#include "common.cuh"
+#include "dense_kernels.cuh"
+#include "philox.cuh"
+#include "sample_kernels.cuh"
+#include "score_kernels.cuh"
+
+using namespace santa;
+
+namespace {
+
+constexpr int kNumSMs = 148;
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct WsLayout {
+  int Cmax = 0, nsplit = 1, max_loc = 1;
+  size_t stash = 0, cstats = 0, partial = 0, tickets = 0, flags = 0, bscores = 0, bern = 0, total = 0;
+};
+
+int elem_bytes(int dtype) { return dtype == SANTA_F32 ? 4 : 2; }
+
+santa_status validate_geometry(const santa_geometry* g) {
+  if (!g) return SANTA_ERR_INVALID_ARG;
+  if (g->batch < 1 || g->n_heads < 1 || g->n_kv_heads < 1) return SANTA_ERR_SHAPE;
+  if (g->n_heads % g->n_kv_heads != 0) return SANTA_ERR_SHAPE;
+  const int G = g->n_heads / g->n_kv_heads;
+  if (!(G == 1 || G == 2 || G == 4 || G == 8)) return SANTA_ERR_UNSUPPORTED;
+  if (g->head_dim != 64 && g->head_dim != 128) return SANTA_ERR_UNSUPPORTED;
+  if (g->dtype != SANTA_BF16 && g->dtype != SANTA_F32 && g->dtype != SANTA_F16) return SANTA_ERR_INVALID_ARG;
+  if (g->max_seqlen < 1) return SANTA_ERR_EMPTY_DISTRIBUTION;
+  if (!(g->scale >= 0.f) || !std::isfinite(g->scale)) return SANTA_ERR_INVALID_ARG;
+  if (g->batch_offset < 0 || g->head_offset < 0) return SANTA_ERR_INVALID_ARG;
+  if (g->page_table) {
+    if (g->page_size < 16 || g->page_size % 16 != 0) return SANTA_ERR_SHAPE;
+    if (g->max_pages_per_seq < (g->max_seqlen + g->page_size - 1) / g->page_size) return SANTA_ERR_SHAPE;
+    if (!aligned16(g->page_table) && (reinterpret_cast<uintptr_t>(g->page_table) & 3u)) return SANTA_ERR_ALIGNMENT;
+  }
+  return SANTA_OK;
+}
+
+WsLayout layout(const santa_geometry* g, int S) {
+  WsLayout L;
+  const int G = g->n_heads / g->n_kv_heads;
+  const size_t B = g->batch, H = g->n_heads, Hkv = g->n_kv_heads, D = g->head_dim;
+  L.Cmax = (g->max_seqlen + kChunk - 1) / kChunk;
+  const int units = g->batch * g->n_kv_heads;
+  int ns = (2 * kNumSMs + units - 1) / units;
+  ns = ns < 1 ? 1 : ns;
+  ns = ns > 64 ? 64 : ns;
+  ns = ns > S ? S : ns;
+  L.nsplit = ns < 1 ? 1 : ns;
+  L.max_loc = (S + L.nsplit - 1) / L.nsplit;
+  size_t off = 0;
+  L.flags = off; off = align256(off + 4);     // flag word at offset 0 (santa_read_error_flags)
+  L.tickets = off; off = align256(off + B * Hkv * 4);  // S-independent offset (seq-shard phases)
+  const size_t stash_bytes = B * H * (size_t)L.Cmax * kChunk * 4;
+  const size_t opart_bytes = B * H * (size_t)L.Cmax * D * 4;   // dense partials share this region
+  L.stash = off; off = align256(off + (stash_bytes > opart_bytes ? stash_bytes : opart_bytes));
+  L.cstats = off; off = align256(off + B * H * (size_t)L.Cmax * 8);
+  L.partial = off; off = align256(off + B * Hkv * (size_t)L.nsplit * G * D * 4);
+  L.bscores = off; off = align256(off + B * H * (size_t)L.Cmax * kChunk * 4);
+  L.bern = off; off = align256(off + B * Hkv * ((size_t)G * D * 4 + D * 4 + 256));  // weights, sel, sel_n
+  L.total = off;
+  return L;
+}
+
+santa_status check_ws(const santa_geometry* g, int S, void* ws, size_t ws_bytes, WsLayout* L) {
+  *L = layout(g, S);
+  if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255u)) return SANTA_ERR_WORKSPACE;
+  if (ws_bytes < L->total) return SANTA_ERR_WORKSPACE;
+  return SANTA_OK;
+}
+
+template <typename P>
+P* at(void* ws, size_t off) { return reinterpret_cast<P*>(reinterpret_cast<char*>(ws) + off); }
+
+KvLayout kv_layout(const santa_geometry* g) {
+  KvLayout kv;
+  kv.page_table = g->page_table;
+  kv.page_size = g->page_table ? g->page_size : g->max_seqlen;
+  kv.max_pages = g->page_table ? g->max_pages_per_seq : 1;
+  kv.n_kv_heads = g->n_kv_heads;
+  return kv;
+}
+
+float scale_log2(const santa_geometry* g) {
+  const float s = g->scale > 0.f ? g->scale : 1.0f / std::sqrt((float)g->head_dim);
+  return s * kLog2e;
+}
+
+santa_status last_cuda() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    return SANTA_ERR_CUDA;
+  }
+  return SANTA_OK;
+}
+
+template <typename Kern, typename... Args>
+cudaError_t launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// ---- dispatch helpers -----------------------------------------------------------------
+template <template <typename, int, int> class F, typename... A>
+santa_status dispatch(int dtype, int D, int G, A&&... a) {
+#define SANTA_G(T, DD)                                        \
+  switch (G) {                                                \
+    case 1: return F<T, DD, 1>::run(a...);                    \
+    case 2: return F<T, DD, 2>::run(a...);                    \
+    case 4: return F<T, DD, 4>::run(a...);                    \
+    case 8: return F<T, DD, 8>::run(a...);                    \
+    default: return SANTA_ERR_UNSUPPORTED;                    \
+  }
+#define SANTA_D(T)                                            \
+  if (D == 64) { SANTA_G(T, 64) } else { SANTA_G(T, 128) }
+  if (dtype == SANTA_BF16) { SANTA_D(__nv_bfloat16) }
+  if (dtype == SANTA_F16) { SANTA_D(__half) }
+  if (dtype == SANTA_F32) { SANTA_D(float) }
+#undef SANTA_D
+#undef SANTA_G
+  return SANTA_ERR_UNSUPPORTED;
+}
+
+struct DecodeArgs {
+  const santa_geometry* g;
+  const void *q, *K, *V;
+  const int32_t* seqlens;
+  int S, mode;
+  uint64_t seed, offset;
+  void* out;
+  float* out_f32;
+  int32_t* idx_out;
+  void* ws;
+  WsLayout L;
+  cudaStream_t st;
+  cudaEvent_t const* events;  // NULL or [3]
+  // seq-shard
+  const double* stats_all;
+  int rank, world;
+  const int32_t* token_offset;
+  bool scores_given;          // Bernoulli path: scores already in ws (bscores) -> stats from them
+};
+
+template <typename T, int D, int G>
+struct RunScore {
+  static santa_status run(const DecodeArgs& a) {
+    ScoreParams p;
+    p.q = a.q;
+    p.K = a.K;
+    p.kv = kv_layout(a.g);
+    p.seqlens = a.seqlens;
+    p.B = a.g->batch;
+    p.H = a.g->n_heads;
+    p.Hkv = a.g->n_kv_heads;
+    p.scale_log2 = scale_log2(a.g);
+    p.stash = at<float>(a.ws, a.L.stash);
+    p.cstats = at<float2>(a.ws, a.L.cstats);
+    p.Cmax = a.L.Cmax;
+    p.stash_stride = a.L.Cmax * kChunk;
+    p.tickets = at<uint32_t>(a.ws, a.L.tickets);
+    p.flags = at<uint32_t>(a.ws, a.L.flags);
+    dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
+    if (a.events) cudaEventRecord(a.events[0], a.st);
+    if (launch(score_stats_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
+      return SANTA_ERR_CUDA;
+    return SANTA_OK;
+  }
+};
+
+template <typename T, int D, int G>
+struct RunSample {
+  static santa_status run(const DecodeArgs& a) {
+    SampleParams p;
+    p.stash = at<float>(a.ws, a.L.stash);
+    p.cstats = at<float2>(a.ws, a.L.cstats);
+    p.Cmax = a.L.Cmax;
+    p.stash_stride = a.L.Cmax * kChunk;
+    p.V = a.V;
+    p.kv = kv_layout(a.g);
+    p.seqlens = a.seqlens;
+    p.B = a.g->batch;
+    p.H = a.g->n_heads;
+    p.Hkv = a.g->n_kv_heads;
+    p.S = a.S;
+    p.mode = a.mode;
+    p.nsplit = a.L.nsplit;
+    p.max_loc = a.L.max_loc;
+    p.seed = a.seed;
+    p.offset = a.offset;
+    p.batch_offset = a.g->batch_offset;
+    p.head_offset = a.g->head_offset;
+    p.out = a.out;
+    p.out_f32 = a.out_f32;
+    p.idx_out = a.idx_out;
+    p.partial = at<float>(a.ws, a.L.partial);
+    p.tickets = at<uint32_t>(a.ws, a.L.tickets);
+    p.flags = at<uint32_t>(a.ws, a.L.flags);
+    p.stats_all = a.stats_all;
+    p.rank = a.rank;
+    p.world = a.world;
+    p.token_offset = a.token_offset;
+    constexpr int EB = (int)sizeof(T);
+    const size_t smem = (size_t)G * a.L.Cmax * 8 + (((size_t)G * a.L.max_loc * 4 + 15) & ~size_t(15)) +
+                        (size_t)(kSampleThreads / (D * EB / 16)) * D * 4;
+    static int configured = 0;
+    if (smem > 48 * 1024 && configured < (int)smem) {
+      if (cudaFuncSetAttribute(sample_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      configured = (int)smem;
+    }
+    if (a.events) cudaEventRecord(a.events[1], a.st);
+    dim3 grid(a.L.nsplit, a.g->n_kv_heads, a.g->batch);
+    if (launch(sample_gather_kernel<T, D, G>, grid, dim3(kSampleThreads), smem, a.st, a.events == nullptr, p) !=
+        cudaSuccess)
+      return SANTA_ERR_CUDA;
+    if (a.events) cudaEventRecord(a.events[2], a.st);
+    return SANTA_OK;
+  }
+};
+
+template <typename T, int D, int G>
+struct RunDense {
+  static santa_status run(const DecodeArgs& a) {
+    DenseParams p;
+    p.q = a.q;
+    p.K = a.K;
+    p.V = a.V;
+    p.kv = kv_layout(a.g);
+    p.seqlens = a.seqlens;
+    p.B = a.g->batch;
+    p.H = a.g->n_heads;
+    p.Hkv = a.g->n_kv_heads;
+    p.scale_log2 = scale_log2(a.g);
+    p.cstats = at<float2>(a.ws, a.L.cstats);
+    p.opart = at<float>(a.ws, a.L.stash);
+    p.Cmax = a.L.Cmax;
+    p.out = a.out;
+    p.flags = at<uint32_t>(a.ws, a.L.flags);
+    dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
+    if (launch(dense_partial_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
+      return SANTA_ERR_CUDA;
+    if (launch(dense_combine_kernel<T, D>, dim3(a.g->n_heads, a.g->batch), dim3(D), 0, a.st, true, p) !=
+        cudaSuccess)
+      return SANTA_ERR_CUDA;
+    return SANTA_OK;
+  }
+};
+
+// local shard combine: (m_r, L_r) per (b, h) from the chunk stats, fp64
+__global__ void shard_combine_kernel(const float2* __restrict__ cstats, const int32_t* __restrict__ seqlens,
+                                     int H, int Cmax, double* __restrict__ stats_out) {
+  pdl_wait_primary();
+  const int h = blockIdx.x, b = blockIdx.y;
+  const int seqlen = __ldg(seqlens + b);
+  const int nC = seqlen > 0 ? (seqlen + kChunk - 1) / kChunk : 0;
+  const float2* cs = cstats + ((size_t)b * H + h) * Cmax;
+  __shared__ double red[32];
+  float m = -INFINITY;
+  for (int c = threadIdx.x; c < nC; c += blockDim.x) m = fmaxf(m, __ldcg(&cs[c].x));
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  float mm = -INFINITY;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mm = fmaxf(mm, (float)red[w]);
+  __syncthreads();
+  double s = 0.0;
+  for (int c = threadIdx.x; c < nC; c += blockDim.x) {
+    const float2 st = __ldcg(&cs[c]);
+    if (st.y > 0.f) s += exp2((double)st.x - (double)mm) * (double)st.y;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];  // fixed order
+    stats_out[((size_t)b * H + h) * 2] = nC ? (double)mm : -INFINITY;
+    stats_out[((size_t)b * H + h) * 2 + 1] = nC ? t : 0.0;
+  }
+}
+
+__global__ void append_kv_kernel(void* K, void* V, const void* kn, const void* vn, KvLayout kv,
+                                 const int32_t* seqlens, int D, int eb) {
+  const int kvh = blockIdx.x, b = blockIdx.y;
+  const int t = __ldg(seqlens + b) - 1;
+  if (t < 0) return;
+  const int64_t dst = kv.row(b, kvh, t, D) * eb;
+  const int64_t src = ((int64_t)b * kv.n_kv_heads + kvh) * D * eb;
+  for (int i = threadIdx.x; i < D * eb; i += blockDim.x) {
+    reinterpret_cast<char*>(K)[dst + i] = reinterpret_cast<const char*>(kn)[src + i];
+    reinterpret_cast<char*>(V)[dst + i] = reinterpret_cast<const char*>(vn)[src + i];
+  }
+}
+
+__global__ void philox_test_kernel(uint64_t seed, uint64_t offset, uint32_t tag, uint32_t h, uint32_t b, int n,
+                                   double* out, uint4 ctr, uint2 key, uint32_t* raw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  PhiloxStream ps(seed, offset, tag, h, b);
+  if (i < n) out[i] = ps.uniform((uint32_t)i);
+  if (raw && i == 0) {
+    const Philox4 o = philox4x32_10(ctr.x, ctr.y, ctr.z, ctr.w, key.x, key.y);
+    raw[0] = o.x[0]; raw[1] = o.x[1]; raw[2] = o.x[2]; raw[3] = o.x[3];
+  }
+}
+
+santa_status validate_decode_ptrs(const void* q, const void* K, const void* V, const int32_t* seqlens,
+                                  const void* out) {
+  if (!q || !K || !V || !seqlens || !out) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(K) || !aligned16(V) || !aligned16(out)) return SANTA_ERR_ALIGNMENT;
+  if (reinterpret_cast<uintptr_t>(seqlens) & 3u) return SANTA_ERR_ALIGNMENT;
+  return SANTA_OK;
+}
+
+template <typename T, int D, int G>
+struct RunBern {
+  // mode 0: standalone scores (scores != NULL, no stash); mode 1: fused into the decode step
+  static santa_status run(const DecodeArgs& a, const void* Kt, int nB, int stratified, int mean_group,
+                          float* scores, uint8_t* mask, bool for_decode) {
+    BernParams p = {};
+    p.q = a.q;
+    p.Kt = Kt;
+    p.seqlens = a.seqlens;
+    p.B = a.g->batch;
+    p.H = a.g->n_heads;
+    p.Hkv = a.g->n_kv_heads;
+    p.nB = nB;
+    p.stratified = stratified;
+    p.mean_group = mean_group;
+    p.seed = a.seed;
+    p.offset = a.offset;
+    p.batch_offset = a.g->batch_offset;
+    p.head_offset = a.g->head_offset;
+    p.scale = a.g->scale > 0.f ? a.g->scale : 1.0f / std::sqrt((float)D);
+    char* bern = at<char>(a.ws, a.L.bern);
+    const size_t units = (size_t)a.g->batch * a.g->n_kv_heads;
+    p.w = reinterpret_cast<float*>(bern);
+    p.sel = reinterpret_cast<int*>(bern + units * G * D * 4);
+    p.sel_n = reinterpret_cast<int*>(bern + units * G * D * 4 + units * D * 4);
+    p.feature_mask = mask;
+    p.page_table = a.g->page_table;
+    p.page_size = a.g->page_size;
+    p.max_pages = a.g->max_pages_per_seq;
+    p.scores = scores;
+    p.score_stride = a.g->max_seqlen;
+    p.stash = for_decode ? at<float>(a.ws, a.L.stash) : nullptr;
+    p.cstats = at<float2>(a.ws, a.L.cstats);
+    p.Cmax = a.L.Cmax;
+    p.stash_stride = a.L.Cmax * kChunk;
+    p.tickets = at<uint32_t>(a.ws, a.L.tickets);
+    p.flags = at<uint32_t>(a.ws, a.L.flags);
+    if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
+        cudaSuccess)
+      return SANTA_ERR_CUDA;
+    if (launch(bern_chunk_kernel<T, D, G>, dim3(a.L.Cmax, a.g->n_kv_heads, a.g->batch), dim3(kScoreThreads), 0,
+               a.st, true, p) != cudaSuccess)
+      return SANTA_ERR_CUDA;
+    return SANTA_OK;
+  }
+};
+
+santa_status validate_bern(const santa_geometry* g, const void* q, const void* Kt, const int32_t* seqlens,
+                           int32_t nB) {
+  if (!q || !Kt || !seqlens) return SANTA_ERR_INVALID_ARG;
+  if (nB < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (nB > 4096) return SANTA_ERR_UNSUPPORTED;
+  if (!aligned16(q) || !aligned16(Kt)) return SANTA_ERR_ALIGNMENT;
+  if (!g->page_table && (g->max_seqlen % 8) != 0) return SANTA_ERR_SHAPE;  // 16-B aligned feature rows
+  return SANTA_OK;
+}
+
+santa_status decode_common(const santa_geometry* g, const void* q, const void* K, const void* V,
+                           const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
+                           void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
+                           void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
+  if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
+  if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 3u)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = mode;
+  a.seed = seed; a.offset = offset; a.out = out; a.idx_out = idx_out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  a.events = reinterpret_cast<cudaEvent_t const*>(events);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* santa_status_string(santa_status s) {
+  switch (s) {
+    case SANTA_OK: return "SANTA_OK";
+    case SANTA_ERR_INVALID_ARG: return "SANTA_ERR_INVALID_ARG";
+    case SANTA_ERR_SHAPE: return "SANTA_ERR_SHAPE";
+    case SANTA_ERR_EMPTY_BUDGET: return "SANTA_ERR_EMPTY_BUDGET";
+    case SANTA_ERR_EMPTY_DISTRIBUTION: return "SANTA_ERR_EMPTY_DISTRIBUTION";
+    case SANTA_ERR_UNSUPPORTED: return "SANTA_ERR_UNSUPPORTED";
+    case SANTA_ERR_WORKSPACE: return "SANTA_ERR_WORKSPACE";
+    case SANTA_ERR_ALIGNMENT: return "SANTA_ERR_ALIGNMENT";
+    case SANTA_ERR_CUDA: return "SANTA_ERR_CUDA";
+  }
+  return "SANTA_ERR_UNKNOWN";
+}
+
+const char* santa_version(void) {
+  return "libsanta 0.1 sm_100a (score_stats:mma.sync-m16n8k16, sample_gather, dense_partial+combine, bernoulli)";
+}
+
+size_t santa_workspace_bytes(const santa_geometry* g, int32_t S) {
+  if (validate_geometry(g) != SANTA_OK || S < 1) return 0;
+  return layout(g, S).total;
+}
+
+santa_status santa_decode_attention(const santa_geometry* g, const void* q, const void* K, const void* V,
+                                    const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
+                                    uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
+                                    void* stream) {
+  return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr, stream);
+}
+
+santa_status santa_decode_attention_profiled(const santa_geometry* g, const void* q, const void* K,
+                                             const void* V, const int32_t* seqlens, int32_t S, int32_t mode,
+                                             uint64_t seed, uint64_t offset, void* out, int32_t* idx_out,
+                                             void* ws, size_t ws_bytes, void* const* events, void* stream) {
+  if (!events || !events[0] || !events[1] || !events[2]) return SANTA_ERR_INVALID_ARG;
+  return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, events, stream);
+}
+
+santa_status santa_dense_reference(const santa_geometry* g, const void* q, const void* K, const void* V,
+                                   const int32_t* seqlens, void* out, void* ws, size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, 1, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K; a.V = V; a.seqlens = seqlens; a.out = out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunDense>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+santa_status santa_bernoulli_scores(const santa_geometry* g, const void* q, const void* Kt, const int32_t* seqlens,
+                                    int32_t nB, int32_t stratified, int32_t mean_group, uint64_t seed,
+                                    uint64_t offset, float* scores, uint8_t* feature_mask, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if ((s = validate_bern(g, q, Kt, seqlens, nB)) != SANTA_OK) return s;
+  if (!scores) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(scores)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, 1, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.seqlens = seqlens; a.seed = seed; a.offset = offset; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunBern>(g->dtype, g->head_dim, G, a, Kt, (int)nB, (int)stratified, (int)mean_group, scores,
+                             feature_mask, false)) != SANTA_OK)
+    return s;
+  return last_cuda();
+}
+
+santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const void* q, const void* Kt, const void* V,
+                                              const int32_t* seqlens, int32_t nB, int32_t stratified,
+                                              int32_t mean_group, int32_t S, int32_t mode, uint64_t seed,
+                                              uint64_t offset, void* out, int32_t* idx_out, void* ws,
+                                              size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if ((s = validate_bern(g, q, Kt, seqlens, nB)) != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
+  if ((s = validate_decode_ptrs(q, Kt, V, seqlens, out)) != SANTA_OK) return s;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = mode; a.seed = seed; a.offset = offset;
+  a.out = out; a.idx_out = idx_out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunBern>(g->dtype, g->head_dim, G, a, Kt, (int)nB, (int)stratified, (int)mean_group,
+                             (float*)nullptr, (uint8_t*)nullptr, true)) != SANTA_OK)
+    return s;
+  if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+santa_status santa_seqshard_stats(const santa_geometry* g, const void* q, const void* K_shard,
+                                  const int32_t* shard_seqlens, double* stats_out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (!q || !K_shard || !shard_seqlens || !stats_out) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(K_shard) || !aligned16(stats_out)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, 1, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K_shard; a.seqlens = shard_seqlens; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  if (launch(shard_combine_kernel, dim3(g->n_heads, g->batch), dim3(128), 0, a.st, true,
+             (const float2*)at<float2>(ws, a.L.cstats), shard_seqlens, g->n_heads, a.L.Cmax, stats_out) !=
+      cudaSuccess)
+    return SANTA_ERR_CUDA;
+  return last_cuda();
+}
+
+santa_status santa_seqshard_sample_gather(const santa_geometry* g, const double* stats_all, int32_t rank,
+                                          int32_t world, const int32_t* token_offset, const void* V_shard,
+                                          const int32_t* shard_seqlens, int32_t S, int32_t mode, uint64_t seed,
+                                          uint64_t offset, float* partial_out, int32_t* idx_out, void* ws,
+                                          size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
+  if (!stats_all || !V_shard || !shard_seqlens || !partial_out || !token_offset) return SANTA_ERR_INVALID_ARG;
+  if (world < 1 || rank < 0 || rank >= world) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(V_shard) || !aligned16(partial_out)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  // phase 2 must see the same chunk layout as phase 1 (which sized it with S = 1)
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.V = V_shard; a.seqlens = shard_seqlens; a.S = S; a.mode = mode; a.seed = seed;
+  a.offset = offset; a.out = partial_out; a.out_f32 = partial_out; a.idx_out = idx_out; a.ws = ws;
+  a.stats_all = stats_all; a.rank = rank; a.world = world; a.token_offset = token_offset;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+santa_status santa_decode_step_host(const santa_geometry* g, const void* q_host, const void* k_new_host,
+                                    const void* v_new_host, void* q_dev, void* k_new_dev, void* v_new_dev,
+                                    void* K, void* V, const int32_t* seqlens, int32_t S, int32_t mode,
+                                    uint64_t seed, uint64_t offset, void* out_dev, void* out_host, void* ws,
+                                    size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (!q_host || !k_new_host || !v_new_host || !q_dev || !k_new_dev || !v_new_dev || !out_host)
+    return SANTA_ERR_INVALID_ARG;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if ((s = validate_decode_ptrs(q_dev, K, V, seqlens, out_dev)) != SANTA_OK) return s;
+  WsLayout L;
+  if ((s = check_ws(g, S, ws, ws_bytes, &L)) != SANTA_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t eb = elem_bytes(g->dtype), D = g->head_dim;
+  const size_t qb = (size_t)g->batch * g->n_heads * D * eb, kb = (size_t)g->batch * g->n_kv_heads * D * eb;
+  if (cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (cudaMemcpyAsync(k_new_dev, k_new_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (cudaMemcpyAsync(v_new_dev, v_new_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, k_new_dev, v_new_dev, kv_layout(g), seqlens,
+                                                                  (int)D, (int)eb);
+  if ((s = last_cuda()) != SANTA_OK) return s;
+  if ((s = decode_common(g, q_dev, K, V, seqlens, S, mode, seed, offset, out_dev, nullptr, ws, ws_bytes, nullptr,
+                         stream)) != SANTA_OK)
+    return s;
+  if (cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
+  return SANTA_OK;
+}
+
+santa_status santa_philox_uniforms(uint64_t seed, uint64_t offset, int32_t tag, int32_t h_global, int32_t b_global,
+                                   int32_t n, double* out, const uint32_t* ctr_key_host, uint32_t* raw_out,
+                                   void* stream) {
+  if (!out || n < 1) return SANTA_ERR_INVALID_ARG;
+  uint4 ctr = make_uint4(0, 0, 0, 0);
+  uint2 key = make_uint2(0, 0);
+  if (ctr_key_host) {
+    ctr = make_uint4(ctr_key_host[0], ctr_key_host[1], ctr_key_host[2], ctr_key_host[3]);
+    key = make_uint2(ctr_key_host[4], ctr_key_host[5]);
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  philox_test_kernel<<<(n + 255) / 256, 256, 0, st>>>(seed, offset, (uint32_t)tag, (uint32_t)h_global,
+                                                      (uint32_t)b_global, n, out, ctr, key, raw_out);
+  return last_cuda();
+}
+
+santa_status santa_read_error_flags(void* ws, uint32_t* flags_out, void* stream) {
+  if (!ws || !flags_out) return SANTA_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) & 255u) return SANTA_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (cudaMemcpy(flags_out, ws, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return SANTA_ERR_CUDA;
+  return SANTA_OK;
+}
+
+}  // extern "C"

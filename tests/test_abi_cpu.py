@@ -1,0 +1,102 @@
+"""C-ABI checks that need no GPU (-m "not gpu"): the library loads, exports every symbol
+include/santa.h declares, sizes its workspace by pure host arithmetic, and rejects invalid
+arguments before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+import torch
+
+from conftest import ROOT
+
+import paper_2605_01910_b200 as santa
+from paper_2605_01910_b200 import _abi
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "santa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(santa_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = _declared()
+    assert len(names) >= 13
+    for n in names:
+        assert hasattr(_abi.LIB, n), n
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump -lelf {santa.LIB_PATH} 2>&1").read()
+    assert "sm_100a" in out and "sm_90" not in out.replace("sm_100a", "")
+    assert "sm_100a" in santa.santa_version()
+
+
+def test_status_strings():
+    for code, name in _abi.STATUS.items():
+        assert _abi.LIB.santa_status_string(code).decode() == name
+
+
+def _geo(**kw):
+    g = _abi.Geometry()
+    g.batch, g.n_heads, g.n_kv_heads, g.head_dim, g.dtype = 1, 32, 8, 128, 0
+    g.max_seqlen, g.scale = 32768, 0.0
+    for k, v in kw.items():
+        setattr(g, k, v)
+    return g
+
+
+def test_workspace_bytes_host_arithmetic():
+    g = _geo()
+    n = santa.santa_workspace_bytes(g, 256)
+    C = 32768 // 256
+    stash = 32 * C * 256 * 4
+    assert stash < n < 3 * stash            # stash + Bernoulli score scratch + small tables
+    assert santa.santa_workspace_bytes(_geo(n_heads=30), 256) == 0     # H % H_kv
+    assert santa.santa_workspace_bytes(_geo(head_dim=96), 256) == 0    # unsupported d
+    assert santa.santa_workspace_bytes(_geo(max_seqlen=0), 256) == 0
+    assert santa.santa_workspace_bytes(g, 0) == 0
+    assert santa.santa_workspace_bytes(_geo(n_heads=128, n_kv_heads=8), 1) == 0   # G = 16
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(n_heads=30), 2), (dict(head_dim=80), 5), (dict(max_seqlen=0), 4), (dict(dtype=9), 1),
+    (dict(batch=0), 2), (dict(n_heads=64, n_kv_heads=4), 5), (dict(scale=float("nan")), 1),
+    (dict(page_table=16, page_size=24, max_pages_per_seq=4096), 2),
+])
+def test_invalid_geometry_rejected_without_gpu(kw, status):
+    g = _geo(**kw)
+    st = _abi.LIB.santa_decode_attention(ctypes.byref(g), 16, 16, 16, 16, 256, 1, 0, 0, 16, None, 256, 1 << 30, None)
+    assert st == status
+
+
+def test_invalid_call_arguments_rejected_without_gpu():
+    g = _geo()
+    L = _abi.LIB
+    assert L.santa_decode_attention(ctypes.byref(g), 16, 16, 16, 16, 0, 1, 0, 0, 16, None, 256, 1 << 30, None) == 3
+    assert L.santa_decode_attention(ctypes.byref(g), 16, 16, 16, 16, 8, 5, 0, 0, 16, None, 256, 1 << 30, None) == 1
+    assert L.santa_decode_attention(ctypes.byref(g), None, 16, 16, 16, 8, 1, 0, 0, 16, None, 256, 1 << 30, None) == 1
+    assert L.santa_decode_attention(ctypes.byref(g), 8, 16, 16, 16, 8, 1, 0, 0, 16, None, 256, 1 << 30, None) == 7
+    assert L.santa_decode_attention(ctypes.byref(g), 16, 16, 16, 16, 8, 1, 0, 0, 16, None, 128, 1 << 30, None) == 6
+    assert L.santa_decode_attention(ctypes.byref(g), 16, 16, 16, 16, 8, 1, 0, 0, 16, None, 256, 1000, None) == 6
+    assert L.santa_bernoulli_scores(ctypes.byref(g), 16, 16, 16, 0, 1, 1, 0, 0, 16, None, 256, 1 << 30, None) == 3
+    assert L.santa_seqshard_sample_gather(ctypes.byref(g), 16, 2, 2, 16, 16, 16, 8, 1, 0, 0, 16, None, 256,
+                                          1 << 30, None) == 1
+    assert L.santa_philox_uniforms(0, 0, 1, 0, 0, 0, 16, None, None, None) == 1
+
+
+def test_binding_refuses_cpu_tensors():
+    q = torch.zeros(1, 4, 128, dtype=torch.bfloat16)
+    K = torch.zeros(1, 1, 16, 128, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):
+        santa.decode(q, K, K, torch.tensor([16], dtype=torch.int32), 4, ws=torch.zeros(1 << 20, dtype=torch.uint8))
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2605_01910_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt), f
