@@ -128,6 +128,19 @@ santa_status santa_decode_attention_profiled(const santa_geometry* geo, const vo
                                              size_t workspace_bytes, void* const* events,
                                              void* stream);
 
+/* The two phases of santa_decode_attention, exposed separately (same arguments and
+ * workspace; calling santa_score_phase then santa_sample_phase on one stream is exactly
+ * santa_decode_attention).  Phase 1 = the split-KV score pass:
+ * it reads every K byte and leaves the per-chunk (m_c, l_c) and the fp32 prefix stash in
+ * `workspace`.  Phase 2 = combine + thresholds + inverse CDF + gather-add (rows a3-a6). */
+santa_status santa_score_phase(const santa_geometry* geo, const void* q, const void* K,
+                               const int32_t* seqlens, void* workspace, size_t workspace_bytes,
+                               void* stream);
+santa_status santa_sample_phase(const santa_geometry* geo, const void* V, const int32_t* seqlens,
+                                int32_t S, int32_t mode, uint64_t seed, uint64_t offset, void* out,
+                                int32_t* idx_out, void* workspace, size_t workspace_bytes,
+                                void* stream);
+
 /* Exact dense decode attention softmax(q K^T * scale) V (Eq. 1) with the same
  * split-KV score pass and a flash-decoding LSE combine; the in-repo reference the SANTA
  * latency is reported against.  Arguments as above. */

@@ -20,7 +20,8 @@ from ._abi import DTYPES, FLAG_EMPTY_SEQ, MODES, Geometry, SantaError
 
 __all__ = [
     "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes",
-    "santa_decode_attention", "santa_decode_attention_profiled", "santa_dense_reference",
+    "santa_decode_attention", "santa_decode_attention_profiled", "santa_score_phase", "santa_sample_phase",
+    "santa_dense_reference",
     "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
     "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_philox_uniforms",
     "santa_read_error_flags", "santa_version", "decode", "dense", "LIB_PATH",
@@ -88,6 +89,17 @@ def santa_decode_attention_profiled(geo, q, K, V, seqlens, S, mode, seed, offset
     _abi.check("santa_decode_attention_profiled", _abi.LIB.santa_decode_attention_profiled(
         ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
         _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), ctypes.cast(ev, ctypes.c_void_p), _stream(stream)))
+
+
+def santa_score_phase(geo, q, K, seqlens, ws, stream=None):
+    _abi.check("santa_score_phase", _abi.LIB.santa_score_phase(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(seqlens), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_sample_phase(geo, V, seqlens, S, mode, seed, offset, out, idx_out, ws, stream=None):
+    _abi.check("santa_sample_phase", _abi.LIB.santa_sample_phase(
+        ctypes.byref(geo), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset, _ptr(out), _ptr(idx_out),
+        _ptr(ws), ws.numel(), _stream(stream)))
 
 
 def santa_dense_reference(geo, q, K, V, seqlens, out, ws, stream=None):

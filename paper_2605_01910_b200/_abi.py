@@ -55,6 +55,8 @@ def _load() -> ctypes.CDLL:
         "santa_decode_attention": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_decode_attention_profiled": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp, vp], i32),
         "santa_dense_reference": ([G, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+        "santa_score_phase": ([G, vp, vp, vp, vp, sz, vp], i32),
+        "santa_sample_phase": ([G, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_bernoulli_scores": ([G, vp, vp, vp, i32, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_decode_attention_bernoulli": ([G, vp, vp, vp, vp, i32, i32, i32, i32, i32, u64, u64, vp, vp, vp,
                                               sz, vp], i32),

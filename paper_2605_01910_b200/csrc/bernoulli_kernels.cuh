@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
 
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams p) {
-  __shared__ __align__(16) float sS[G * kChunk];
-  __shared__ __align__(16) float sAcc[4][G][kChunk];
+  __shared__ __align__(16) float sS[G * kDenseChunk];
+  __shared__ __align__(16) float sAcc[4][G][kDenseChunk];
   __shared__ float sW[G][D];
   __shared__ int sSel[D];
   pdl_wait_primary();
@@ -140,17 +140,17 @@ __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams
     if (b == 0 && kvh == 0 && p.flags) *p.flags = 0u;
   }
   const int seqlen = __ldg(p.seqlens + b);
-  const int chunk_start = c * kChunk;
-  const int n_valid = min(kChunk, seqlen - chunk_start);
+  const int chunk_start = c * kDenseChunk;
+  const int n_valid = min(kDenseChunk, seqlen - chunk_start);
   const size_t unit = (size_t)b * p.Hkv + kvh;
   const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
   float2* cst = p.cstats + bh0 * p.Cmax + c;
   if (n_valid <= 0) {
     if (threadIdx.x < G) cst[(size_t)threadIdx.x * p.Cmax] = make_float2(-INFINITY, 0.f);
     if (p.scores && chunk_start < p.score_stride)
-      for (int t = threadIdx.x; t < G * kChunk; t += kScoreThreads) {
-        const int k = chunk_start + t % kChunk;
-        if (k < p.score_stride) p.scores[(bh0 + t / kChunk) * p.score_stride + k] = 0.f;
+      for (int t = threadIdx.x; t < G * kDenseChunk; t += kScoreThreads) {
+        const int k = chunk_start + t % kDenseChunk;
+        if (k < p.score_stride) p.scores[(bh0 + t / kDenseChunk) * p.score_stride + k] = 0.f;
       }
     return;
   }
@@ -203,16 +203,18 @@ __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams
     for (int e = 0; e < 8; ++e) sAcc[warp][g][kl + e] = acc[g][e];
   __syncthreads();
   const float sl2 = p.scale * kLog2e;
-  for (int t = threadIdx.x; t < G * kChunk; t += kScoreThreads) {
-    const int g = t / kChunk, k = t % kChunk;
+  for (int t = threadIdx.x; t < G * kDenseChunk; t += kScoreThreads) {
+    const int g = t / kDenseChunk, k = t % kDenseChunk;
     const float ph = ((sAcc[0][g][k] + sAcc[1][g][k]) + sAcc[2][g][k]) + sAcc[3][g][k];
     const bool valid = k < n_valid;
-    sS[g * kChunk + k] = valid ? ph * sl2 : -INFINITY;
+    sS[g * kDenseChunk + k] = valid ? ph * sl2 : -INFINITY;
     if (p.scores && chunk_start + k < p.score_stride)
       p.scores[(bh0 + g) * p.score_stride + chunk_start + k] = valid ? ph * p.scale : 0.f;
   }
   __syncthreads();
-  if (p.stash) chunk_stats_prefix<G>(sS, p.stash + bh0 * p.stash_stride + chunk_start, p.stash_stride, cst, p.Cmax);
+  if (p.stash)
+    chunk_epilogue<G>(sS, kDenseChunk, n_valid, warp, 4, p.stash + bh0 * p.stash_stride + chunk_start,
+                      p.stash_stride, cst, p.Cmax);
 }
 
 }  // namespace santa

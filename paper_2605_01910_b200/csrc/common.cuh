@@ -9,7 +9,6 @@
 
 namespace santa {
 
-constexpr int kChunk = 256;        // split-KV chunk length L (keys per score CTA)
 constexpr int kScoreThreads = 128; // 4 warps per score CTA
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -41,6 +40,12 @@ __device__ __forceinline__ uint4 ldg_nc(const void* p) {
   asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ float4 ldcg_f4(const void* p) {
+  float4 r;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
   return r;
 }
 
@@ -96,11 +101,19 @@ struct KvLayout {
   int32_t page_size;
   int32_t max_pages;
   int32_t n_kv_heads;
+  int32_t page_shift;         // log2(page_size) if a power of two, else -1 (paged only)
   // element offset of row `t` (token) of (b, kvh); the row is D contiguous elements
   __device__ __forceinline__ int64_t row(int b, int kvh, int t, int D) const {
-    int page = t / page_size;
-    int within = t - page * page_size;
-    int64_t phys = page_table ? (int64_t)__ldg(page_table + (int64_t)b * max_pages + page) : b;
+    if (!page_table) return (((int64_t)b * n_kv_heads + kvh) * page_size + t) * D;
+    int page, within;
+    if (page_shift >= 0) {
+      page = t >> page_shift;
+      within = t & (page_size - 1);
+    } else {
+      page = t / page_size;
+      within = t - page * page_size;
+    }
+    const int64_t phys = (int64_t)__ldg(page_table + (int64_t)b * max_pages + page);
     return ((phys * n_kv_heads + kvh) * (int64_t)page_size + within) * D;
   }
 };

@@ -28,14 +28,14 @@ struct DenseParams {
 
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(kScoreThreads, 3) dense_partial_kernel(DenseParams p) {
-  __shared__ __align__(16) float sS[G * kChunk];
+  __shared__ __align__(16) float sS[G * kDenseChunk];
   __shared__ __align__(16) float sO[4][G][D];
   pdl_launch_dependents();
   const int c = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
   if (c == 0 && b == 0 && kvh == 0 && threadIdx.x == 0 && p.flags) *p.flags = 0u;
   const int seqlen = __ldg(p.seqlens + b);
-  const int chunk_start = c * kChunk;
-  const int n_valid = min(kChunk, seqlen - chunk_start);
+  const int chunk_start = c * kDenseChunk;
+  const int n_valid = min(kDenseChunk, seqlen - chunk_start);
   const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
   float2* cst = p.cstats + bh0 * p.Cmax + c;
   if (n_valid <= 0) {
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kScoreThreads, 3) dense_partial_kernel(DensePa
   for (int h = warp; h < G; h += 4) {
     float v[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = sS[h * kChunk + 8 * lane + e];
+    for (int e = 0; e < 8; ++e) v[e] = sS[h * kDenseChunk + 8 * lane + e];
     float m = v[0];
 #pragma unroll
     for (int e = 1; e < 8; ++e) m = fmaxf(m, v[e]);
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kScoreThreads, 3) dense_partial_kernel(DensePa
     for (int e = 0; e < 8; ++e) {
       v[e] = ex2(v[e] - m);
       sum += v[e];
-      sS[h * kChunk + 8 * lane + e] = v[e];
+      sS[h * kDenseChunk + 8 * lane + e] = v[e];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kScoreThreads, 3) dense_partial_kernel(DensePa
     for (int u = 0; u < U; ++u) {
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const float w = sS[g * kChunk + k0 + u];
+        const float w = sS[g * kDenseChunk + k0 + u];
 #pragma unroll
         for (int e = 0; e < EPL; ++e) acc[g][e] = fmaf(w, vv[u][e], acc[g][e]);
       }
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(D) dense_combine_kernel(DenseParams p) {
     if (threadIdx.x == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
     return;
   }
-  const int nC = (seqlen + kChunk - 1) / kChunk;
+  const int nC = (seqlen + kDenseChunk - 1) / kDenseChunk;
   const float2* cs = p.cstats + bh * p.Cmax;
   float ms = -INFINITY;
   for (int c = 0; c < nC; ++c) ms = fmaxf(ms, __ldcg(&cs[c].x));

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 
+#include <cudaTypedefs.h>
+
 #include "bernoulli_kernels.cuh"
 #include "common.cuh"
 #include "dense_kernels.cuh"
@@ -15,15 +17,16 @@ using namespace santa;
 
 namespace {
 
-constexpr int kNumSMs = 148;
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct WsLayout {
-  int Cmax = 0, nsplit = 1, max_loc = 1;
-  size_t stash = 0, cstats = 0, partial = 0, tickets = 0, flags = 0, bscores = 0, bern = 0, total = 0;
+  int L = 64, Cmax = 0, Cmax256 = 0;
+  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, bern = 0, total = 0;
 };
+
+constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 1024 chunks of <= 1024 keys
 
 int elem_bytes(int dtype) { return dtype == SANTA_F32 ? 4 : 2; }
 
@@ -36,6 +39,7 @@ santa_status validate_geometry(const santa_geometry* g) {
   if (g->head_dim != 64 && g->head_dim != 128) return SANTA_ERR_UNSUPPORTED;
   if (g->dtype != SANTA_BF16 && g->dtype != SANTA_F32 && g->dtype != SANTA_F16) return SANTA_ERR_INVALID_ARG;
   if (g->max_seqlen < 1) return SANTA_ERR_EMPTY_DISTRIBUTION;
+  if (g->max_seqlen > kMaxSeqlen) return SANTA_ERR_UNSUPPORTED;
   if (!(g->scale >= 0.f) || !std::isfinite(g->scale)) return SANTA_ERR_INVALID_ARG;
   if (g->batch_offset < 0 || g->head_offset < 0) return SANTA_ERR_INVALID_ARG;
   if (g->page_table) {
@@ -50,23 +54,21 @@ WsLayout layout(const santa_geometry* g, int S) {
   WsLayout L;
   const int G = g->n_heads / g->n_kv_heads;
   const size_t B = g->batch, H = g->n_heads, Hkv = g->n_kv_heads, D = g->head_dim;
-  L.Cmax = (g->max_seqlen + kChunk - 1) / kChunk;
-  const int units = g->batch * g->n_kv_heads;
-  int ns = (2 * kNumSMs + units - 1) / units;
-  ns = ns < 1 ? 1 : ns;
-  ns = ns > 64 ? 64 : ns;
-  ns = ns > S ? S : ns;
-  L.nsplit = ns < 1 ? 1 : ns;
-  L.max_loc = (S + L.nsplit - 1) / L.nsplit;
+  // SANTA chunk length: the smallest multiple of 64 keeping <= 1024 chunks per sequence
+  // (fine-grained work for the persistent score pass, bounded CDF tables for the sampler)
+  L.L = 64;
+  while ((g->max_seqlen + L.L - 1) / L.L > 1024) L.L *= 2;
+  L.Cmax = (g->max_seqlen + L.L - 1) / L.L;
+  L.Cmax256 = (g->max_seqlen + 255) / 256;  // dense reference / Bernoulli chunking
   size_t off = 0;
   L.flags = off; off = align256(off + 4);     // flag word at offset 0 (santa_read_error_flags)
   L.tickets = off; off = align256(off + B * Hkv * 4);  // S-independent offset (seq-shard phases)
-  const size_t stash_bytes = B * H * (size_t)L.Cmax * kChunk * 4;
-  const size_t opart_bytes = B * H * (size_t)L.Cmax * D * 4;   // dense partials share this region
+  const size_t keys = (size_t)L.Cmax * L.L > (size_t)L.Cmax256 * 256 ? (size_t)L.Cmax * L.L : (size_t)L.Cmax256 * 256;
+  const size_t stash_bytes = B * H * keys * 4;
+  const size_t opart_bytes = B * H * (size_t)L.Cmax256 * D * 4;   // dense partials share this region
   L.stash = off; off = align256(off + (stash_bytes > opart_bytes ? stash_bytes : opart_bytes));
-  L.cstats = off; off = align256(off + B * H * (size_t)L.Cmax * 8);
-  L.partial = off; off = align256(off + B * Hkv * (size_t)L.nsplit * G * D * 4);
-  L.bscores = off; off = align256(off + B * H * (size_t)L.Cmax * kChunk * 4);
+  const size_t cmx = L.Cmax > L.Cmax256 ? L.Cmax : L.Cmax256;
+  L.cstats = off; off = align256(off + B * H * cmx * 8);
   L.bern = off; off = align256(off + B * Hkv * ((size_t)G * D * 4 + D * 4 + 256));  // weights, sel, sel_n
   L.total = off;
   return L;
@@ -88,6 +90,12 @@ KvLayout kv_layout(const santa_geometry* g) {
   kv.page_size = g->page_table ? g->page_size : g->max_seqlen;
   kv.max_pages = g->page_table ? g->max_pages_per_seq : 1;
   kv.n_kv_heads = g->n_kv_heads;
+  kv.page_shift = -1;
+  if (g->page_table && (g->page_size & (g->page_size - 1)) == 0) {
+    int s = 0;
+    while ((1 << s) < g->page_size) ++s;
+    kv.page_shift = s;
+  }
   return kv;
 }
 
@@ -157,8 +165,46 @@ struct DecodeArgs {
   const double* stats_all;
   int rank, world;
   const int32_t* token_offset;
-  bool scores_given;          // Bernoulli path: scores already in ws (bscores) -> stats from them
+  int Lc = 0, Cc = 0;         // chunking the sampler reads (0 => the SANTA layout L / Cmax)
 };
+
+int num_sms() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// K viewed as a 2-D tensor [rows][D] (D contiguous); 64 x 64-element boxes, 128B swizzle.
+bool make_kmap(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, dtype == SANTA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void*>(K), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 template <typename T, int D, int G>
 struct RunScore {
@@ -175,13 +221,49 @@ struct RunScore {
     p.stash = at<float>(a.ws, a.L.stash);
     p.cstats = at<float2>(a.ws, a.L.cstats);
     p.Cmax = a.L.Cmax;
-    p.stash_stride = a.L.Cmax * kChunk;
+    p.L = a.L.L;
+    p.stash_stride = a.L.Cmax * a.L.L;
     p.tickets = at<uint32_t>(a.ws, a.L.tickets);
     p.flags = at<uint32_t>(a.ws, a.L.flags);
-    dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
     if (a.events) cudaEventRecord(a.events[0], a.st);
-    if (launch(score_stats_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
-      return SANTA_ERR_CUDA;
+    const bool stream = !a.g->page_table || a.g->page_size % kStageKeys == 0;
+    if constexpr (sizeof(T) == 2) if (stream) {
+      CUtensorMap tm;
+      const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
+                                            : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
+      if (!make_kmap(&tm, a.K, rows, D, a.g->dtype)) return SANTA_ERR_CUDA;
+      constexpr size_t kStageBytes = (D / 64) * 8192;
+      constexpr int NW = kStreamWarps, SPW = kStreamSlots;
+      const size_t smem = 1024 + (size_t)NW * G * p.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
+      if (smem <= 220 * 1024) {  // else: per-warp score buffers too large (G * L big) -> fallback kernel
+      static size_t configured = 0;
+      if (smem > configured) {
+        if (cudaFuncSetAttribute(score_stream_kernel<T, D, G, NW, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+          return SANTA_ERR_CUDA;
+        configured = smem;
+      }
+      const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
+      const int grid = total < num_sms() ? total : num_sms();
+      if (launch(score_stream_kernel<T, D, G, NW, SPW>, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p) !=
+          cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
+      }
+    }
+    {
+      dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
+      const size_t smem = (size_t)G * p.L * 4;
+      static size_t configured = 0;
+      if (smem > 48 * 1024 && smem > configured) {
+        if (cudaFuncSetAttribute(score_chunk_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+          return SANTA_ERR_CUDA;
+        configured = smem;
+      }
+      if (launch(score_chunk_kernel<T, D, G>, grid, dim3(128), smem, a.st, false, p) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+    }
     return SANTA_OK;
   }
 };
@@ -192,8 +274,9 @@ struct RunSample {
     SampleParams p;
     p.stash = at<float>(a.ws, a.L.stash);
     p.cstats = at<float2>(a.ws, a.L.cstats);
-    p.Cmax = a.L.Cmax;
-    p.stash_stride = a.L.Cmax * kChunk;
+    p.Cmax = a.Cc ? a.Cc : a.L.Cmax;
+    p.L = a.Lc ? a.Lc : a.L.L;
+    p.stash_stride = p.Cmax * p.L;
     p.V = a.V;
     p.kv = kv_layout(a.g);
     p.seqlens = a.seqlens;
@@ -202,8 +285,6 @@ struct RunSample {
     p.Hkv = a.g->n_kv_heads;
     p.S = a.S;
     p.mode = a.mode;
-    p.nsplit = a.L.nsplit;
-    p.max_loc = a.L.max_loc;
     p.seed = a.seed;
     p.offset = a.offset;
     p.batch_offset = a.g->batch_offset;
@@ -211,28 +292,48 @@ struct RunSample {
     p.out = a.out;
     p.out_f32 = a.out_f32;
     p.idx_out = a.idx_out;
-    p.partial = at<float>(a.ws, a.L.partial);
-    p.tickets = at<uint32_t>(a.ws, a.L.tickets);
     p.flags = at<uint32_t>(a.ws, a.L.flags);
     p.stats_all = a.stats_all;
     p.rank = a.rank;
     p.world = a.world;
     p.token_offset = a.token_offset;
-    constexpr int EB = (int)sizeof(T);
-    const size_t smem = (size_t)G * a.L.Cmax * 8 + (((size_t)G * a.L.max_loc * 4 + 15) & ~size_t(15)) +
-                        (size_t)(kSampleThreads / (D * EB / 16)) * D * 4;
-    static int configured = 0;
-    if (smem > 48 * 1024 && configured < (int)smem) {
+    p.trace = nullptr;
+    // CTAs per head: a thread-block cluster of CS CTAs splits the S strata (more SMs on the
+    // latency-bound search/gather), partials summed through DSMEM.  Aim at >= ~2 CTAs per SM.
+    int CS = 1;
+    const int heads = a.g->batch * a.g->n_heads;
+    while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
+    p.cluster = CS;
+    const size_t smem = (size_t)p.Cmax * 16 + (size_t)a.S * 16 + (size_t)(kSampleThreads / 16 + 1) * D * 4 + 64;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
       if (cudaFuncSetAttribute(sample_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem) != cudaSuccess)
         return SANTA_ERR_CUDA;
-      configured = (int)smem;
+      configured = smem;
     }
     if (a.events) cudaEventRecord(a.events[1], a.st);
-    dim3 grid(a.L.nsplit, a.g->n_kv_heads, a.g->batch);
-    if (launch(sample_gather_kernel<T, D, G>, grid, dim3(kSampleThreads), smem, a.st, a.events == nullptr, p) !=
-        cudaSuccess)
-      return SANTA_ERR_CUDA;
+    const bool pdl = a.events == nullptr && a.stats_all == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
+    cfg.blockDim = dim3(kSampleThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CS;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (pdl) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelEx(&cfg, sample_gather_kernel<T, D, G>, p) != cudaSuccess) return SANTA_ERR_CUDA;
     if (a.events) cudaEventRecord(a.events[2], a.st);
     return SANTA_OK;
   }
@@ -253,10 +354,10 @@ struct RunDense {
     p.scale_log2 = scale_log2(a.g);
     p.cstats = at<float2>(a.ws, a.L.cstats);
     p.opart = at<float>(a.ws, a.L.stash);
-    p.Cmax = a.L.Cmax;
+    p.Cmax = a.L.Cmax256;
     p.out = a.out;
     p.flags = at<uint32_t>(a.ws, a.L.flags);
-    dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
+    dim3 grid(a.L.Cmax256, a.g->n_kv_heads, a.g->batch);
     if (launch(dense_partial_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
       return SANTA_ERR_CUDA;
     if (launch(dense_combine_kernel<T, D>, dim3(a.g->n_heads, a.g->batch), dim3(D), 0, a.st, true, p) !=
@@ -268,11 +369,11 @@ struct RunDense {
 
 // local shard combine: (m_r, L_r) per (b, h) from the chunk stats, fp64
 __global__ void shard_combine_kernel(const float2* __restrict__ cstats, const int32_t* __restrict__ seqlens,
-                                     int H, int Cmax, double* __restrict__ stats_out) {
+                                     int H, int Cmax, int L, double* __restrict__ stats_out) {
   pdl_wait_primary();
   const int h = blockIdx.x, b = blockIdx.y;
   const int seqlen = __ldg(seqlens + b);
-  const int nC = seqlen > 0 ? (seqlen + kChunk - 1) / kChunk : 0;
+  const int nC = seqlen > 0 ? (seqlen + L - 1) / L : 0;
   const float2* cs = cstats + ((size_t)b * H + h) * Cmax;
   __shared__ double red[32];
   float m = -INFINITY;
@@ -365,14 +466,14 @@ struct RunBern {
     p.score_stride = a.g->max_seqlen;
     p.stash = for_decode ? at<float>(a.ws, a.L.stash) : nullptr;
     p.cstats = at<float2>(a.ws, a.L.cstats);
-    p.Cmax = a.L.Cmax;
-    p.stash_stride = a.L.Cmax * kChunk;
+    p.Cmax = a.L.Cmax256;
+    p.stash_stride = a.L.Cmax256 * kDenseChunk;
     p.tickets = at<uint32_t>(a.ws, a.L.tickets);
     p.flags = at<uint32_t>(a.ws, a.L.flags);
     if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
         cudaSuccess)
       return SANTA_ERR_CUDA;
-    if (launch(bern_chunk_kernel<T, D, G>, dim3(a.L.Cmax, a.g->n_kv_heads, a.g->batch), dim3(kScoreThreads), 0,
+    if (launch(bern_chunk_kernel<T, D, G>, dim3(a.L.Cmax256, a.g->n_kv_heads, a.g->batch), dim3(kScoreThreads), 0,
                a.st, true, p) != cudaSuccess)
       return SANTA_ERR_CUDA;
     return SANTA_OK;
@@ -396,6 +497,7 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
   if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
   if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
   if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 3u)) return SANTA_ERR_ALIGNMENT;
@@ -431,7 +533,7 @@ const char* santa_status_string(santa_status s) {
 }
 
 const char* santa_version(void) {
-  return "libsanta 0.1 sm_100a (score_stats:mma.sync-m16n8k16, sample_gather, dense_partial+combine, bernoulli)";
+  return "libsanta 0.2 sm_100a (score_stream: TMA 128B-swizzle ring + mma.sync m16n8k16, persistent; score_chunk fallback; sample_gather per (b,h); dense_partial+combine; bernoulli)";
 }
 
 size_t santa_workspace_bytes(const santa_geometry* g, int32_t S) {
@@ -452,6 +554,41 @@ santa_status santa_decode_attention_profiled(const santa_geometry* g, const void
                                              void* ws, size_t ws_bytes, void* const* events, void* stream) {
   if (!events || !events[0] || !events[1] || !events[2]) return SANTA_ERR_INVALID_ARG;
   return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, events, stream);
+}
+
+santa_status santa_score_phase(const santa_geometry* g, const void* q, const void* K, const int32_t* seqlens,
+                               void* ws, size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (!q || !K || !seqlens) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(q) || !aligned16(K)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, 1, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K; a.seqlens = seqlens; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+santa_status santa_sample_phase(const santa_geometry* g, const void* V, const int32_t* seqlens, int32_t S,
+                                int32_t mode, uint64_t seed, uint64_t offset, void* out, int32_t* idx_out, void* ws,
+                                size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
+  if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
+  if (!V || !seqlens || !out) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(V) || !aligned16(out)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = mode; a.seed = seed; a.offset = offset; a.out = out;
+  a.idx_out = idx_out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
 }
 
 santa_status santa_dense_reference(const santa_geometry* g, const void* q, const void* K, const void* V,
@@ -497,6 +634,7 @@ santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const voi
   if (s != SANTA_OK) return s;
   if ((s = validate_bern(g, q, Kt, seqlens, nB)) != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
   if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
   if ((s = validate_decode_ptrs(q, Kt, V, seqlens, out)) != SANTA_OK) return s;
   DecodeArgs a = {};
@@ -508,6 +646,8 @@ santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const voi
   if ((s = dispatch<RunBern>(g->dtype, g->head_dim, G, a, Kt, (int)nB, (int)stratified, (int)mean_group,
                              (float*)nullptr, (uint8_t*)nullptr, true)) != SANTA_OK)
     return s;
+  a.Lc = kDenseChunk;
+  a.Cc = a.L.Cmax256;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   return last_cuda();
 }
@@ -526,7 +666,7 @@ santa_status santa_seqshard_stats(const santa_geometry* g, const void* q, const 
   const int G = g->n_heads / g->n_kv_heads;
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if (launch(shard_combine_kernel, dim3(g->n_heads, g->batch), dim3(128), 0, a.st, true,
-             (const float2*)at<float2>(ws, a.L.cstats), shard_seqlens, g->n_heads, a.L.Cmax, stats_out) !=
+             (const float2*)at<float2>(ws, a.L.cstats), shard_seqlens, g->n_heads, a.L.Cmax, a.L.L, stats_out) !=
       cudaSuccess)
     return SANTA_ERR_CUDA;
   return last_cuda();
@@ -540,6 +680,7 @@ santa_status santa_seqshard_sample_gather(const santa_geometry* g, const double*
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
   if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
   if (!stats_all || !V_shard || !shard_seqlens || !partial_out || !token_offset) return SANTA_ERR_INVALID_ARG;
   if (world < 1 || rank < 0 || rank >= world) return SANTA_ERR_INVALID_ARG;
