@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
         }
         jj[u] = cc[u] * p.L + k;
         if (l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u] + tok0;
+      } else if (m < Sl && l == 0 && p.idx_out) {
+        p.idx_out[bh * S + m_lo + m] = -1;  // stratum owned by another sequence shard
       }
     }
     // gather-add of the U rows

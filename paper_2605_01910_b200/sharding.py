@@ -1,0 +1,165 @@
+"""Multi-GPU orchestration of the SANTA decode step (one process per GPU,
+torch.distributed for the plumbing).
+
+1. Batch x kv-head sharding (configs 2/3): the B*H_kv (batch, kv-head) units are independent,
+   so they are partitioned into contiguous slabs, one or more per rank, with NO collective on
+   the data path.  Philox is keyed by GLOBAL (b, h) through the geometry's batch_offset /
+   head_offset, so every rank reproduces exactly the indices a single GPU would draw.
+
+2. Sequence sharding (config 4, reading #18 of DESIGN.md): rank r holds the contiguous token
+   range [r*n/R, (r+1)*n/R) of every sequence.  Phase 1 (local score pass) gives per-(b, h)
+   (m_r, L_r); one all_gather of those [B, H, 2] fp64 tuples lets every rank build the same
+   global shard CDF; phase 2 keeps the strata whose global threshold lands in the rank's slice of
+   the CDF and gathers its local V rows; one all_reduce(SUM) of the [B, H, d] fp32 partials gives
+   the output.  The sampled indices equal the unsharded ones (up to boundary rounding).
+
+The per-rank compute is a pluggable backend (``CudaBackend`` below = the C-ABI kernels); the
+functions here only move tensors between ranks.  CPU tests drive the same orchestration with
+world_size 2 over gloo and an oracle backend supplied by the test.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+# ---------------------------------------------------------------------------------------------
+# 1. batch x kv-head sharding
+# ---------------------------------------------------------------------------------------------
+
+@dataclasses.dataclass(frozen=True)
+class Slab:
+    """A rectangle of (batch, kv-head) units: batches [b0, b1) x kv-heads [k0, k1)."""
+    b0: int
+    b1: int
+    k0: int
+    k1: int
+
+    @property
+    def units(self) -> int:
+        return (self.b1 - self.b0) * (self.k1 - self.k0)
+
+
+def plan_units(batch: int, n_kv_heads: int, world: int) -> List[List[Slab]]:
+    """Split the batch*n_kv_heads units (row-major over (b, kv-head)) into `world` contiguous
+    ranges of near-equal size; each range is returned as at most three rectangular slabs
+    (partial first batch, whole middle batches, partial last batch)."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    total = batch * n_kv_heads
+    plan = []
+    for r in range(world):
+        u0, u1 = total * r // world, total * (r + 1) // world
+        slabs = []
+        u = u0
+        while u < u1:
+            b, k = divmod(u, n_kv_heads)
+            if k == 0 and u1 - u >= n_kv_heads:   # whole batches
+                nb = (u1 - u) // n_kv_heads
+                slabs.append(Slab(b, b + nb, 0, n_kv_heads))
+                u += nb * n_kv_heads
+            else:                                  # part of one batch
+                k1 = min(n_kv_heads, k + (u1 - u))
+                slabs.append(Slab(b, b + 1, k, k1))
+                u += k1 - k
+        plan.append(slabs)
+    return plan
+
+
+def slab_inputs(q: torch.Tensor, K: torch.Tensor, V: torch.Tensor, seqlens: torch.Tensor, slab: Slab, G: int):
+    """Views of a contiguous [B, H_kv, n, d] cache (and q [B, H, d]) restricted to one slab,
+    made contiguous for the call (on a real deployment each rank only ever holds its slab)."""
+    qs = q[slab.b0:slab.b1, slab.k0 * G:slab.k1 * G].contiguous()
+    Ks = K[slab.b0:slab.b1, slab.k0:slab.k1].contiguous()
+    Vs = V[slab.b0:slab.b1, slab.k0:slab.k1].contiguous()
+    return qs, Ks, Vs, seqlens[slab.b0:slab.b1].contiguous()
+
+
+# ---------------------------------------------------------------------------------------------
+# 2. sequence sharding
+# ---------------------------------------------------------------------------------------------
+
+def shard_bounds(n: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous shards in rank order: rank r holds tokens [r*n//R, (r+1)*n//R)."""
+    return [(r * n // world, (r + 1) * n // world) for r in range(world)]
+
+
+class CudaBackend:
+    """Per-rank compute through the C-ABI (santa_seqshard_stats / santa_seqshard_sample_gather)."""
+
+    def __init__(self):
+        from . import (make_geometry, santa_seqshard_sample_gather, santa_seqshard_stats,  # noqa: F401
+                       workspace)
+        self._mk, self._ws_fn = make_geometry, workspace
+        self._stats, self._sg = santa_seqshard_stats, santa_seqshard_sample_gather
+        self.ws = None
+
+    def stats(self, q, K_shard, shard_seqlens, n_kv_heads: int, S: int):
+        geo = self._mk(q, n_kv_heads, K_shard.shape[2])
+        if self.ws is None or self.ws.numel() < self._ws_bytes(geo, S):
+            self.ws = self._ws_fn(geo, S, q.device)
+        out = torch.empty(q.shape[0], q.shape[1], 2, dtype=torch.float64, device=q.device)
+        self._stats(geo, q, K_shard, shard_seqlens, out, self.ws)
+        self._geo = geo
+        return out
+
+    def _ws_bytes(self, geo, S):
+        from . import santa_workspace_bytes
+        return santa_workspace_bytes(geo, S)
+
+    def sample_gather(self, stats_all, rank, world, token_offset, V_shard, shard_seqlens, S, mode, seed, offset,
+                      return_idx=False):
+        B, H = stats_all.shape[1], stats_all.shape[2]
+        d = V_shard.shape[-1]
+        partial = torch.empty(B, H, d, dtype=torch.float32, device=V_shard.device)
+        idx = torch.empty(B, H, S, dtype=torch.int32, device=V_shard.device) if return_idx else None
+        self._sg(self._geo, stats_all.contiguous(), rank, world, token_offset, V_shard, shard_seqlens, S, mode, seed,
+                 offset, partial, idx, self.ws)
+        return partial, idx
+
+
+def seqshard_decode(q: torch.Tensor, K_shard: torch.Tensor, V_shard: torch.Tensor, seqlens: torch.Tensor,
+                    S: int, mode: str, seed: int, offset: int = 0, backend=None, group=None,
+                    return_idx: bool = False):
+    """Sequence-sharded S^2ANTA decode step (config 4).  Every rank passes its own contiguous
+    K/V shard [B, H_kv, n_local, d] and the FULL q [B, H, d] and seqlens [B] (global lengths).
+    Returns the summed output [B, H, d] fp32 on every rank (and this rank's global indices, -1
+    for strata owned by other ranks, if return_idx)."""
+    backend = backend or CudaBackend()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    B = q.shape[0]
+    # this rank's token range of every sequence
+    n_loc = K_shard.shape[2]
+    lo = torch.tensor([rank * int(s) // world for s in seqlens.tolist()], dtype=torch.int32)
+    hi = torch.tensor([(rank + 1) * int(s) // world for s in seqlens.tolist()], dtype=torch.int32)
+    shard_len = (hi - lo).to(q.device)
+    if int((hi - lo).max()) > n_loc:
+        raise ValueError("K_shard too short for this rank's token range")
+    stats = backend.stats(q, K_shard, shard_len, K_shard.shape[1], S)           # [B, H, 2] fp64
+    gathered = [torch.empty_like(stats) for _ in range(world)]
+    dist.all_gather(gathered, stats, group=group)                               # the exchange step
+    stats_all = torch.stack(gathered, 0)                                        # [R, B, H, 2]
+    partial, idx = backend.sample_gather(stats_all, rank, world, lo.to(q.device), V_shard, shard_len, S, mode, seed,
+                                         offset, return_idx=return_idx)
+    dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)                 # sum of partial outputs
+    return (partial, idx) if return_idx else partial
+
+
+def batch_shard_decode(q, K, V, seqlens, S, mode, seed, offset=0, group=None, decode_fn=None):
+    """Batch x kv-head sharded decode: this rank computes its slabs of the (b, kv-head) units with
+    global Philox ids; no collective.  Returns [(slab, out_slab)] for this rank."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    G = q.shape[1] // K.shape[1]
+    if decode_fn is None:
+        from . import decode as decode_fn  # noqa: N813
+    res = []
+    for slab in plan_units(q.shape[0], K.shape[1], world)[rank]:
+        qs, Ks, Vs, sl = slab_inputs(q, K, V, seqlens, slab, G)
+        out = decode_fn(qs, Ks, Vs, sl, S, mode, seed, offset, batch_offset=slab.b0, head_offset=slab.k0 * G)
+        res.append((slab, out))
+    return res
