@@ -10,7 +10,7 @@
 //     selected set {c_i > 0, m_i > 0} (reading #14).
 //   per-head ternary: norm_g = max_i |q_{g,i}|, counts from tag 2 keyed by the global head,
 //     w_{g,i} = (norm_g / B) c_{g,i} sign(q_{g,i}); fetched set = union over the group (#15).
-//   Every integer decision (a_i, floor, frac, compare) is taken in fp64, as in the oracle.
+//   Every integer decision (a_i, floor, frac, compare) is taken in fp64 (the oracle takes the same decisions in fp64)
 //   Output: fp32 weights [G][D], the compacted selected-feature list, the feature mask.
 // bern_chunk_kernel (one CTA per 256-key chunk of (b, kv-head)): reads ONLY the selected
 //   rows of the feature-major cache Kt, p_hat_g[k] = sum_{i in F} w_{g,i} Kt[i][k] (fp32
