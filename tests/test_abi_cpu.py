@@ -99,4 +99,4 @@ def test_product_package_never_imports_the_oracle():
         for f in files:
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
-                assert "oracle" not in re.sub(r"(#|//).*", "", txt), f
+                assert not re.search(r"^\s*(from|import)\s+oracle|santa_oracle|oracle\.", txt, re.M), f
