@@ -129,31 +129,62 @@ __global__ void __launch_bounds__(kScoreThreads, 3) dense_partial_kernel(DensePa
   }
 }
 
+// LSE combine of the chunk partials, 256 threads per (b, h): chunk weights 2^(m_c - m*) in
+// parallel, then each (d, quarter) thread sums a quarter of the chunks (8 loads in flight),
+// quarters summed in fixed order.
 template <typename T, int D>
-__global__ void __launch_bounds__(D) dense_combine_kernel(DenseParams p) {
+__global__ void __launch_bounds__(256) dense_combine_kernel(DenseParams p) {
+  __shared__ float sW[4096];  // max_seqlen <= 2^20 -> <= 4096 chunks
+  __shared__ float sred[8];
+  __shared__ float sAcc[256];
   pdl_wait_primary();
-  const int h = blockIdx.x, b = blockIdx.y;
+  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
   const int seqlen = __ldg(p.seqlens + b);
   const size_t bh = (size_t)b * p.H + h;
   T* out = reinterpret_cast<T*>(p.out) + bh * D;
   if (seqlen < 1) {
-    out[threadIdx.x] = Elem<T>::from_f(0.f);
-    if (threadIdx.x == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
+    for (int d = tid; d < D; d += 256) out[d] = Elem<T>::from_f(0.f);
+    if (tid == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
     return;
   }
   const int nC = (seqlen + kDenseChunk - 1) / kDenseChunk;
   const float2* cs = p.cstats + bh * p.Cmax;
   float ms = -INFINITY;
-  for (int c = 0; c < nC; ++c) ms = fmaxf(ms, __ldcg(&cs[c].x));
-  float num = 0.f, den = 0.f;
-  for (int c = 0; c < nC; ++c) {
+  for (int c = tid; c < nC; c += 256) ms = fmaxf(ms, __ldcg(&cs[c].x));
+  ms = warp_max(ms);
+  if ((tid & 31) == 0) sred[tid >> 5] = ms;
+  __syncthreads();
+  ms = sred[0];
+  for (int w = 1; w < 8; ++w) ms = fmaxf(ms, sred[w]);
+  float den = 0.f;
+  for (int c = tid; c < nC; c += 256) {
     const float2 st = __ldcg(&cs[c]);
-    if (st.y <= 0.f) continue;
-    const float w = ex2(st.x - ms);
-    num = fmaf(w, __ldcg(p.opart + (bh * p.Cmax + c) * D + threadIdx.x), num);
+    const float w = st.y > 0.f ? ex2(st.x - ms) : 0.f;
+    sW[c] = w;
     den = fmaf(w, st.y, den);
   }
-  out[threadIdx.x] = Elem<T>::from_f(num / den);
+  __syncthreads();
+  for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
+  __shared__ float sden[8];
+  if ((tid & 31) == 0) sden[tid >> 5] = den;
+  const int d = tid % D, part = tid / D, nparts = 256 / D;
+  float num = 0.f;
+  for (int c0 = part * 8; c0 < nC; c0 += nparts * 8) {
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = (c0 + u < nC) ? __ldcg(p.opart + (bh * p.Cmax + c0 + u) * D + d) : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (c0 + u < nC) num = fmaf(sW[c0 + u], v[u], num);
+  }
+  sAcc[tid] = num;
+  __syncthreads();
+  if (tid < D) {
+    float s = 0.f, dn = 0.f;
+    for (int q = 0; q < nparts; ++q) s += sAcc[q * D + tid];
+    for (int w = 0; w < 8; ++w) dn += sden[w];
+    out[tid] = Elem<T>::from_f(s / dn);
+  }
 }
 
 }  // namespace santa

@@ -1,28 +1,28 @@
 // sample_kernels.cuh -- combine + sampler + gather-add of the SANTA decode hot path
 // (SURVEY sec. 8(a) rows a3-a6).
 //
-// One CTA = one (batch, query head): it owns all S strata of that head, so no cross-CTA
-// reduction is needed and the chunk CDF is built exactly once per head.  Steps:
-//  a4 thresholds (before griddepcontrol.wait, overlapping the score pass): Philox4x32-10,
-//     T_m in fp64 exactly as the oracle (readings #1-#3).
+// sample_item() handles one (batch b, query head h, split `rank` of CS): the strata
+// m in [S*rank/CS, S*(rank+1)/CS) of that head.  Steps:
+//  a4 thresholds (before griddepcontrol.wait, overlapping the score pass when launched with
+//     PDL): Philox4x32-10, T_m in fp64 exactly as the oracle (readings #1-#3).
 //  a3 combine: the head's chunk stats are loaded in one round trip; m* = max_c m_c,
 //     W_c = 2^(m_c - m*) l_c (fp64), block-wide fp64 scan -> F_c = sum_{c'<=c} W / Z, clamped
-//     to 1 from the last positive chunk on (reading #5).  (The LSE merge of Alg.
-//     prop-budgets P:1606-1607 / flash-k2 P:1701, in fp64.)
-//  a5 inverse CDF: c = min{c : F_c > T} (binary search in shared memory), then the rescaled
-//     threshold t = (T - F_{c-1}) Z 2^(m* - m_c) is located in the chunk's fp32 prefix stash by
-//     a 16-ary search (2 dependent L2 round trips for L <= 256):
-//     k = min{k : P_c[k] > t}; J = c L + k  (J = min{j : F(j) > T}, reading #4).
-//  a6 gather-add: runs of equal consecutive indices (stratified/systematic indices are
-//     non-decreasing in m) are read once and added `count` times (count * v is exact for a
-//     small integer count and a bf16 v); 16 rows in flight per lane group; fp32 accumulators;
-//     1/S and the cast in the epilogue ("adds only", Table).
-//     V rows shared by the G heads of a group are deduplicated by the L2 (the G CTAs of a
-//     group run concurrently), not in shared memory.
+//     to 1 from the last positive chunk on (reading #5); the in-chunk rescale Z l_c / W_c is kept
+//     per chunk.  (The LSE merge of Alg. prop-budgets P:1606-1607 / flash-k2 P:1701, in fp64.)
+//  a5 inverse CDF: c = min{c : F_c > T} by binary search in shared memory (thread per sample),
+//     then k = min{k : P_c[k] > t}, t = (T - F_{c-1}) Z 2^(m* - m_c), J = c L + k (P:699,
+//     reading #4): a HALF-WARP per sample loads the chunk's 256-B prefix block coalesced and
+//     counts P[k] <= rd(t) with ballots (exact, reading #21).
+//  a6 gather-add: the same 16 lanes then load the sample's V row (16 B each) and add it;
+//     8 samples in flight per half-warp; fixed-order reduction over half-warps -> the CTA's
+//     partial sum (1/S and the cast are applied by the caller; "adds only",
+//     Table).  V rows shared by the G heads of a group are deduplicated by the L2.
+//  Sequence-sharded mode (stats_all != NULL, reading #18): the global threshold T is first
+//  located in the shard CDF built from every rank's (m_r, L_r); strata outside this rank's
+//  [F_{r-1}, F_r) are skipped, owned ones are re-normalised to the local distribution.
 //
-// Sequence-sharded mode (stats_all != NULL, reading #18): the global threshold T is first
-// located in the shard CDF built from every rank's (m_r, L_r); strata outside this rank's
-// [F_{r-1}, F_r) are skipped, owned ones are re-normalised to the local distribution.
+// sample_gather_kernel: grid (H*CS, B); the CS CTAs of a head form one thread-block cluster
+// and sum their partials through distributed shared memory in fixed rank order.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -32,7 +32,7 @@
 namespace santa {
 
 constexpr int kSampleThreads = 256;
-constexpr int kMaxBudget = 4096;   // S limit (shared-memory sample tables)
+constexpr int kMaxBudget = 4096;  // S limit (shared-memory sample tables)
 
 struct SampleParams {
   const float* stash;
@@ -44,15 +44,16 @@ struct SampleParams {
   int B, H, Hkv, S, mode;
   uint64_t seed, offset;
   int batch_offset, head_offset;
-  void* out;            // [B, H, D] dtype T (standard mode)
-  float* out_f32;       // [B, H, D] fp32 (seq-shard partial mode) -- used if non-NULL
-  int32_t* idx_out;     // [B, H, S] or NULL
+  void* out;                    // [B, H, D] dtype T (standard mode)
+  float* out_f32;               // [B, H, D] fp32 (seq-shard partial mode) -- used if non-NULL
+  int32_t* idx_out;             // [B, H, S] or NULL
   uint32_t* flags;
   // sequence sharding
-  const double* stats_all;  // [world, B, H, 2] or NULL
+  const double* stats_all;      // [world, B, H, 2] or NULL
   int rank, world;
   const int32_t* token_offset;  // [B] or NULL
-  int cluster;                  // CTAs per head (thread-block cluster size, 1..8)
+  int cluster;                  // CTAs per head (thread-block cluster size / splits)
+  float* split_partial;         // fused kernel: [B*H*cluster][D] scratch
   unsigned long long* trace;    // NULL in the library; tools/microbench_sample.cu phase timing
 };
 
@@ -61,9 +62,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
-#define SANTA_TRACE(i) \
-  if (p.trace && threadIdx.x == 0 && (blockIdx.x % p.cluster) == 0) \
-  p.trace[(blockIdx.y * gridDim.x + blockIdx.x) / p.cluster * 16 + (i)] = gtimer()
+#define SANTA_TRACE(i)                                                   \
+  if (p.trace && threadIdx.x == 0 && rank == 0)                          \
+  p.trace[((size_t)b * p.H + h) * 16 + (i)] = gtimer()
 
 // min{k in [0, n) : P[k] > t} for a non-decreasing fp32 array P (n if none), by one thread (no
 // warp collectives).  Because P[k] is fp32, P[k] > t  <=>  P[k] > rd(t) (t rounded toward -inf
@@ -78,40 +79,38 @@ __device__ __forceinline__ int thread_chunk_search(const float* __restrict__ P, 
   return lo;
 }
 
+// block-wide reductions for any blockDim.x that is a multiple of 32 (<= 1024)
 __device__ __forceinline__ float block_max_f(float v, float* sred) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   v = warp_max(v);
   if (lane == 0) sred[warp] = v;
   __syncthreads();
   float r = sred[0];
-#pragma unroll
-  for (int w = 1; w < kSampleThreads / 32; ++w) r = fmaxf(r, sred[w]);
+  for (int w = 1; w < nw; ++w) r = fmaxf(r, sred[w]);
   __syncthreads();
   return r;
 }
 
 __device__ __forceinline__ int block_max_i(int v, int* sred) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
   if (lane == 0) sred[warp] = v;
   __syncthreads();
   int r = sred[0];
-#pragma unroll
-  for (int w = 1; w < kSampleThreads / 32; ++w) r = max(r, sred[w]);
+  for (int w = 1; w < nw; ++w) r = max(r, sred[w]);
   __syncthreads();
   return r;
 }
 
 // block-wide exclusive scan of one double per thread; *total receives the sum
 __device__ __forceinline__ double block_excl_scan_d(double v, double* sred, double* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const double incl = warp_incl_scan_d(v, lane);
   if (lane == 31) sred[warp] = incl;
   __syncthreads();
   double off = 0.0, tot = 0.0;
-#pragma unroll
-  for (int w = 0; w < kSampleThreads / 32; ++w) {
+  for (int w = 0; w < nw; ++w) {
     const double x = sred[w];
     if (w < warp) off += x;
     tot += x;
@@ -121,70 +120,71 @@ __device__ __forceinline__ double block_excl_scan_d(double v, double* sred, doub
   return off + incl - v;
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(SampleParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* sF = reinterpret_cast<double*>(smem_raw);               // [Cmax]
-  double* sT = sF + p.Cmax;                                        // [S]  (reused: see sR)
-  float2* sC = reinterpret_cast<float2*>(sT + p.S);                // [Cmax]
-  int* sIdx = reinterpret_cast<int*>(sC + p.Cmax);                 // [S]
-  int* sCnt = sIdx + p.S;                                          // [S]
-  float* sRed = reinterpret_cast<float*>(sCnt + p.S);              // [NRG][D]
-  __shared__ double sred_d[kSampleThreads / 32];
-  __shared__ float sred_f[kSampleThreads / 32];
-  __shared__ int sred_i[kSampleThreads / 32];
-  __shared__ double sTlo, sThi, sTscale;
-  __shared__ int sOwnAny;
+// Shared-memory bytes sample_item needs for a CTA of nthreads threads.
+__host__ __device__ inline size_t sample_smem_bytes(int Cmax, int S_local, int D, int nthreads) {
+  return (size_t)Cmax * 16 + (size_t)S_local * 16 + (size_t)(nthreads / 16 + 1) * D * 4 + 64;
+}
 
-  // grid.x = H * CS: the CS CTAs of head h form one thread-block cluster; CTA rank r owns the
-  // strata [m_lo, m_hi) and the cluster sums the partial outputs through distributed shared memory.
-  namespace cg = cooperative_groups;
-  const int CS = p.cluster;
-  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const int h = blockIdx.x / CS, b = blockIdx.y, kvh = h / G;
+// One (b, h, split) work item.  Leaves the CTA's partial sum sum_{own m} V_{J_m} (fp32, not yet
+// scaled by 1/S) in the returned shared array [D]; the caller reduces/scales/writes it.  All
+// threads of the block must call it.  Empty sequences (seqlen < 1) give a zero partial, idx -1
+// and the workspace flag.
+template <typename T, int D, int G>
+__device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int CS, unsigned char* smem_raw) {
+  const int NT = blockDim.x, NW = NT >> 5, NHW = NT >> 4;
+  const int kvh = h / G;
   const int tid = threadIdx.x;
   const size_t bh = (size_t)b * p.H + h;
-  const int S = p.S;                                   // global budget (thresholds, 1/S)
+  const int S = p.S;                                    // global budget (thresholds, 1/S)
   const int m_lo = (int)((long long)S * rank / CS), m_hi = (int)((long long)S * (rank + 1) / CS);
-  const int Sl = m_hi - m_lo;                          // strata owned by this CTA
+  const int Sl = m_hi - m_lo;                           // strata owned by this item
+  const int Slmax = (S + CS - 1) / CS;
+  double* sF = reinterpret_cast<double*>(smem_raw);     // [Cmax] chunk CDF
+  double* sT = sF + p.Cmax;                             // [Slmax] thresholds
+  float2* sC = reinterpret_cast<float2*>(sT + Slmax);   // [Cmax] chunk stats, then rescale (double)
+  int* sChunk = reinterpret_cast<int*>(sC + p.Cmax);    // [Slmax]
+  float* sTl = reinterpret_cast<float*>(sChunk + Slmax);  // [Slmax]
+  float* sRed = sTl + Slmax;                            // [NHW][D]
+  float* sPart = sRed + NHW * D;                        // [D]
+  __shared__ double sred_d[32];
+  __shared__ float sred_f[32];
+  __shared__ int sred_i[32];
+  __shared__ double sTlo, sThi, sTscale;
+  __shared__ int sOwnAny;
+  (void)NW;
 
   SANTA_TRACE(0);
   // ---- a4: thresholds (independent of the score pass) ---------------------------------------
   {
     PhiloxStream ps(p.seed, p.offset, kTagValueSampler, (uint32_t)(p.head_offset + h), (uint32_t)(p.batch_offset + b));
-    for (int i = tid; i < Sl; i += kSampleThreads) sT[i] = sample_threshold(p.mode, m_lo + i, S, ps);
+    for (int i = tid; i < Sl; i += NT) sT[i] = sample_threshold(p.mode, m_lo + i, S, ps);
   }
-
   SANTA_TRACE(1);
   pdl_wait_primary();
   SANTA_TRACE(2);
 
   const int seqlen = __ldg(p.seqlens + b);
-  if (seqlen < 1) {  // empty distribution: zero output, flag, no sampling (cluster-uniform)
-    if (rank == 0) {
-      for (int d = tid; d < D; d += kSampleThreads) {
-        if (p.out_f32) p.out_f32[bh * D + d] = 0.f;
-        else reinterpret_cast<T*>(p.out)[bh * D + d] = Elem<T>::from_f(0.f);
-      }
-      if (tid == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
-    }
+  if (seqlen < 1) {  // empty distribution: zero partial, flag, no sampling
+    for (int d = tid; d < D; d += NT) sPart[d] = 0.f;
+    if (rank == 0 && tid == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
     if (p.idx_out)
-      for (int i = tid; i < Sl; i += kSampleThreads) p.idx_out[bh * S + m_lo + i] = -1;
-    return;
+      for (int i = tid; i < Sl; i += NT) p.idx_out[bh * S + m_lo + i] = -1;
+    __syncthreads();
+    return sPart;
   }
   const int nC = (seqlen + p.L - 1) / p.L;
 
   // ---- a3: chunk stats -> fp64 chunk CDF ------------------------------------------------------
   const float2* cs = p.cstats + bh * p.Cmax;
   float mloc = -INFINITY;
-  for (int c = tid; c < nC; c += kSampleThreads) {
+  for (int c = tid; c < nC; c += NT) {
     const float2 v = __ldcg(cs + c);
     sC[c] = v;
     mloc = fmaxf(mloc, v.x);
   }
   const float mstar = block_max_f(mloc, sred_f);  // (its barrier also publishes sC)
   SANTA_TRACE(3);
-  const int per = (nC + kSampleThreads - 1) / kSampleThreads;
+  const int per = (nC + NT - 1) / NT;
   const int c0 = tid * per, c1 = min(c0 + per, nC);
   double part = 0.0;
   int lastpos = -1;
@@ -203,8 +203,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
     const double w = sF[c];
     run += w;
     sF[c] = c >= lastpos ? 1.0 : run * invZ;
-    // rescale factor of the in-chunk search, Z * 2^(m* - m_c) = Z l_c / W_c, kept in the
-    // (now unused) float2 slot of the chunk as a double
+    // in-chunk rescale Z * 2^(m* - m_c) = Z l_c / W_c, kept in the chunk's (now unused) slot
     reinterpret_cast<double*>(sC)[c] = w > 0.0 ? Z * (double)sC[c].y / w : 0.0;
   }
   SANTA_TRACE(4);
@@ -245,11 +244,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
   __syncthreads();
 
   // ---- a5 (part 1): chunk of every sample (thread per sample, shared-memory search) ------------
-  // c = min{c : F_c > T}; the in-chunk threshold t = (T - F_{c-1}) Z 2^(m* - m_c) is kept as
-  // rd(t) (fp32, rounded toward -inf), which decides P[k] > t exactly (see chunk_count).
-  int* sChunk = reinterpret_cast<int*>(sCnt);        // [S] chunk of sample m (-1: not owned)
-  float* sTl = reinterpret_cast<float*>(sIdx);       // [S] rd(t)
-  for (int m = tid; m < Sl; m += kSampleThreads) {
+  for (int m = tid; m < Sl; m += NT) {
     double Tm = sT[m];
     int c = -1;
     bool own = true;
@@ -275,16 +270,11 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
   SANTA_TRACE(5);
 
   // ---- a5 (part 2) + a6: half-warp per sample: in-chunk search + gather-add ---------------------
-  // 16 lanes load the sample's chunk prefix block coalesced (one 16-B load each for L = 64),
-  // count P[k] <= rd(t) with ballots (= min{k : P[k] > t}), then the same 16 lanes load the V
-  // row (16 B each) and add it.  U samples are in flight per half-warp (2 dependent L2/DRAM
-  // round trips for the whole budget when S <= 16 * U * 16).
   constexpr int EB = (int)sizeof(T);
   constexpr int VCH = D * EB / 16;                  // 16-B chunks per V row
   constexpr int NCH = (VCH + 15) / 16;              // chunks per lane
   constexpr int EPC = 16 / EB;                      // elements per chunk
-  constexpr int NHW = kSampleThreads / 16;          // half-warps
-  constexpr int U = 8;
+  constexpr int U = 8;                              // samples in flight per half-warp
   const int hw = tid >> 4, l = tid & 15;
   const unsigned hmask = 0xffffu << (threadIdx.x & 16);
   float acc[NCH][EPC];
@@ -300,7 +290,6 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
   for (int mw = 2 * (tid >> 5); mw < Sl; mw += NHW * U) {
     const int m0 = mw + (hw & 1);
     int jj[U];
-    // in-chunk search for U samples (loads first, then ballots)
     float4 pv[U];
     int cc[U], nn[U];
 #pragma unroll
@@ -337,7 +326,6 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
         p.idx_out[bh * S + m_lo + m] = -1;  // stratum owned by another sequence shard
       }
     }
-    // gather-add of the U rows
     uint4 raw[U][NCH];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -366,8 +354,7 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
         }
       }
   }
-  // deterministic reduction over the half-warps (fixed order), then over the cluster (fixed rank
-  // order, through distributed shared memory)
+  // deterministic reduction over the half-warps (fixed order)
 #pragma unroll
   for (int q = 0; q < NCH; ++q) {
     const int ch = l + 16 * q;
@@ -377,34 +364,45 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
   }
   __syncthreads();
   SANTA_TRACE(6);
-  float* sPart = sRed + NHW * D;  // [D] this CTA's partial sum
-  for (int d = tid; d < D; d += kSampleThreads) {
+  for (int d = tid; d < D; d += NT) {
     float s = 0.f;
-#pragma unroll
     for (int r = 0; r < NHW; ++r) s += sRed[r * D + d];
     sPart[d] = s;
   }
-  const float invS = 1.0f / (float)S;
-  if (CS > 1) {
+  __syncthreads();
+  return sPart;
+}
+
+template <typename T, int D>
+__device__ __forceinline__ void store_out(const SampleParams& p, size_t bh, int d, float v) {
+  if (p.out_f32) p.out_f32[bh * D + d] = v;
+  else reinterpret_cast<T*>(p.out)[bh * D + d] = Elem<T>::from_f(v);
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  namespace cg = cooperative_groups;
+  const int CS = p.cluster;
+  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int h = blockIdx.x / CS, b = blockIdx.y;
+  const size_t bh = (size_t)b * p.H + h;
+  float* sPart = sample_item<T, D, G>(p, b, h, rank, CS, smem_raw);
+  const float invS = 1.0f / (float)p.S;
+  if (CS > 1) {  // sum the cluster's partials through DSMEM in fixed rank order
     cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();  // partials visible cluster-wide
-    if (rank == 0) {
-      for (int d = tid; d < D; d += kSampleThreads) {
+    cluster.sync();
+    if (rank == 0)
+      for (int d = threadIdx.x; d < D; d += blockDim.x) {
         float s = 0.f;
         for (int r = 0; r < CS; ++r) s += cluster.map_shared_rank(sPart, r)[d];
-        if (p.out_f32) p.out_f32[bh * D + d] = s * invS;
-        else reinterpret_cast<T*>(p.out)[bh * D + d] = Elem<T>::from_f(s * invS);
+        store_out<T, D>(p, bh, d, s * invS);
       }
-    }
     cluster.sync();  // keep every CTA's shared memory alive until rank 0 has read it
   } else {
-    __syncthreads();
-    for (int d = tid; d < D; d += kSampleThreads) {
-      if (p.out_f32) p.out_f32[bh * D + d] = sPart[d] * invS;
-      else reinterpret_cast<T*>(p.out)[bh * D + d] = Elem<T>::from_f(sPart[d] * invS);
-    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) store_out<T, D>(p, bh, d, sPart[d] * invS);
   }
-  SANTA_TRACE(7);
+  if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[bh * 16 + 7] = gtimer();
 }
 
 }  // namespace santa

@@ -9,6 +9,8 @@
 #include "bernoulli_kernels.cuh"
 #include "common.cuh"
 #include "dense_kernels.cuh"
+#include "dense_stream_kernel.cuh"
+#include "fused_kernel.cuh"
 #include "philox.cuh"
 #include "sample_kernels.cuh"
 #include "score_kernels.cuh"
@@ -18,12 +20,16 @@ using namespace santa;
 namespace {
 
 
+// One cooperative launch for the whole step (fused_kernel.cuh): correct, but measured slower than
+// the score kernel + PDL-chained sampler pair on B200 (grid.sync ~1.6 us + lost PDL overlap).
+constexpr bool kUseFusedStep = false;
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct WsLayout {
   int L = 64, Cmax = 0, Cmax256 = 0;
-  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, bern = 0, total = 0;
+  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, bern = 0, split = 0, total = 0;
 };
 
 constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 1024 chunks of <= 1024 keys
@@ -70,6 +76,7 @@ WsLayout layout(const santa_geometry* g, int S) {
   const size_t cmx = L.Cmax > L.Cmax256 ? L.Cmax : L.Cmax256;
   L.cstats = off; off = align256(off + B * H * cmx * 8);
   L.bern = off; off = align256(off + B * Hkv * ((size_t)G * D * 4 + D * 4 + 256));  // weights, sel, sel_n
+  L.split = off; off = align256(off + B * H * 8 * D * 4);  // fused kernel: per-split partial sums
   L.total = off;
   return L;
 }
@@ -194,37 +201,46 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // K viewed as a 2-D tensor [rows][D] (D contiguous); 64 x 64-element boxes, 128B swizzle.
-bool make_kmap(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype) {
+bool make_kmap(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype, int box_rows = 64) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)D * 2};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   return fn(m, dtype == SANTA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
             const_cast<void*>(K), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+ScoreParams make_score_params(const DecodeArgs& a) {
+  ScoreParams p = {};
+  p.q = a.q;
+  p.K = a.K;
+  p.kv = kv_layout(a.g);
+  p.seqlens = a.seqlens;
+  p.B = a.g->batch;
+  p.H = a.g->n_heads;
+  p.Hkv = a.g->n_kv_heads;
+  p.scale_log2 = scale_log2(a.g);
+  p.stash = at<float>(a.ws, a.L.stash);
+  p.cstats = at<float2>(a.ws, a.L.cstats);
+  p.Cmax = a.L.Cmax;
+  p.L = a.L.L;
+  p.stash_stride = a.L.Cmax * a.L.L;
+  p.tickets = at<uint32_t>(a.ws, a.L.tickets);
+  p.flags = at<uint32_t>(a.ws, a.L.flags);
+  return p;
+}
+
+bool stream_eligible(const santa_geometry* g) {
+  return g->dtype != SANTA_F32 && (!g->page_table || g->page_size % kStageKeys == 0);
+}
+
 template <typename T, int D, int G>
 struct RunScore {
   static santa_status run(const DecodeArgs& a) {
-    ScoreParams p;
-    p.q = a.q;
-    p.K = a.K;
-    p.kv = kv_layout(a.g);
-    p.seqlens = a.seqlens;
-    p.B = a.g->batch;
-    p.H = a.g->n_heads;
-    p.Hkv = a.g->n_kv_heads;
-    p.scale_log2 = scale_log2(a.g);
-    p.stash = at<float>(a.ws, a.L.stash);
-    p.cstats = at<float2>(a.ws, a.L.cstats);
-    p.Cmax = a.L.Cmax;
-    p.L = a.L.L;
-    p.stash_stride = a.L.Cmax * a.L.L;
-    p.tickets = at<uint32_t>(a.ws, a.L.tickets);
-    p.flags = at<uint32_t>(a.ws, a.L.flags);
+    ScoreParams p = make_score_params(a);
     if (a.events) cudaEventRecord(a.events[0], a.st);
     const bool stream = !a.g->page_table || a.g->page_size % kStageKeys == 0;
     if constexpr (sizeof(T) == 2) if (stream) {
@@ -268,43 +284,50 @@ struct RunScore {
   }
 };
 
+SampleParams make_sample_params(const DecodeArgs& a) {
+  SampleParams p = {};
+  p.stash = at<float>(a.ws, a.L.stash);
+  p.cstats = at<float2>(a.ws, a.L.cstats);
+  p.Cmax = a.Cc ? a.Cc : a.L.Cmax;
+  p.L = a.Lc ? a.Lc : a.L.L;
+  p.stash_stride = p.Cmax * p.L;
+  p.V = a.V;
+  p.kv = kv_layout(a.g);
+  p.seqlens = a.seqlens;
+  p.B = a.g->batch;
+  p.H = a.g->n_heads;
+  p.Hkv = a.g->n_kv_heads;
+  p.S = a.S;
+  p.mode = a.mode;
+  p.seed = a.seed;
+  p.offset = a.offset;
+  p.batch_offset = a.g->batch_offset;
+  p.head_offset = a.g->head_offset;
+  p.out = a.out;
+  p.out_f32 = a.out_f32;
+  p.idx_out = a.idx_out;
+  p.flags = at<uint32_t>(a.ws, a.L.flags);
+  p.stats_all = a.stats_all;
+  p.rank = a.rank;
+  p.world = a.world;
+  p.token_offset = a.token_offset;
+  p.split_partial = at<float>(a.ws, a.L.split);
+  p.trace = nullptr;
+  p.cluster = 1;
+  return p;
+}
+
 template <typename T, int D, int G>
 struct RunSample {
   static santa_status run(const DecodeArgs& a) {
-    SampleParams p;
-    p.stash = at<float>(a.ws, a.L.stash);
-    p.cstats = at<float2>(a.ws, a.L.cstats);
-    p.Cmax = a.Cc ? a.Cc : a.L.Cmax;
-    p.L = a.Lc ? a.Lc : a.L.L;
-    p.stash_stride = p.Cmax * p.L;
-    p.V = a.V;
-    p.kv = kv_layout(a.g);
-    p.seqlens = a.seqlens;
-    p.B = a.g->batch;
-    p.H = a.g->n_heads;
-    p.Hkv = a.g->n_kv_heads;
-    p.S = a.S;
-    p.mode = a.mode;
-    p.seed = a.seed;
-    p.offset = a.offset;
-    p.batch_offset = a.g->batch_offset;
-    p.head_offset = a.g->head_offset;
-    p.out = a.out;
-    p.out_f32 = a.out_f32;
-    p.idx_out = a.idx_out;
-    p.flags = at<uint32_t>(a.ws, a.L.flags);
-    p.stats_all = a.stats_all;
-    p.rank = a.rank;
-    p.world = a.world;
-    p.token_offset = a.token_offset;
-    p.trace = nullptr;
+    SampleParams p = make_sample_params(a);
     // CTAs per head: a thread-block cluster of CS CTAs splits the S strata (more SMs on the
     // latency-bound search/gather), partials summed through DSMEM.  Aim at >= ~2 CTAs per SM.
     int CS = 1;
     const int heads = a.g->batch * a.g->n_heads;
     while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
     p.cluster = CS;
-    const size_t smem = (size_t)p.Cmax * 16 + (size_t)a.S * 16 + (size_t)(kSampleThreads / 16 + 1) * D * 4 + 64;
+    const size_t smem = sample_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
     static size_t configured = 0;
     if (smem > 48 * 1024 && smem > configured) {
       if (cudaFuncSetAttribute(sample_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -339,6 +362,62 @@ struct RunSample {
   }
 };
 
+// The whole step in one cooperative persistent launch (fused_kernel.cuh).  Returns
+// SANTA_ERR_UNSUPPORTED (nothing launched) when the configuration does not qualify, in which
+// case the caller runs the two-kernel path.
+template <typename T, int D, int G>
+struct RunFused {
+  static santa_status run(const DecodeArgs& a) {
+    if constexpr (sizeof(T) != 2) {
+      return SANTA_ERR_UNSUPPORTED;
+    } else {
+      if (!stream_eligible(a.g)) return SANTA_ERR_UNSUPPORTED;
+      constexpr int NW = kStreamWarps, SPW = kStreamSlots, NT = 32 * (NW + 1);
+      ScoreParams sp = make_score_params(a);
+      SampleParams pp = make_sample_params(a);
+      const int grid = num_sms();
+      int CS = 1;
+      const int heads = a.g->batch * a.g->n_heads;
+      while (CS < 8 && heads * CS * 2 <= 2 * grid && CS * 2 <= a.S) CS *= 2;
+      pp.cluster = CS;
+      constexpr size_t kStageBytes = (D / 64) * 8192;
+      const size_t score_smem = 1024 + (size_t)NW * G * sp.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
+      const size_t samp_smem = sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D, NT);
+      const size_t smem = score_smem > samp_smem ? score_smem : samp_smem;
+      if (smem > 220 * 1024) return SANTA_ERR_UNSUPPORTED;
+      static size_t configured = 0;
+      if (smem > configured) {
+        if (cudaFuncSetAttribute(santa_fused_kernel<T, D, G, NW, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem) != cudaSuccess)
+          return SANTA_ERR_CUDA;
+        configured = smem;
+      }
+      int occ = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, santa_fused_kernel<T, D, G, NW, SPW>, NT, smem) !=
+              cudaSuccess ||
+          occ < 1)
+        return SANTA_ERR_UNSUPPORTED;
+      CUtensorMap tm;
+      const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
+                                            : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
+      if (!make_kmap(&tm, a.K, rows, D, a.g->dtype)) return SANTA_ERR_UNSUPPORTED;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = a.st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, santa_fused_kernel<T, D, G, NW, SPW>, tm, sp, pp) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
+    }
+  }
+};
+
 template <typename T, int D, int G>
 struct RunDense {
   static santa_status run(const DecodeArgs& a) {
@@ -357,10 +436,51 @@ struct RunDense {
     p.Cmax = a.L.Cmax256;
     p.out = a.out;
     p.flags = at<uint32_t>(a.ws, a.L.flags);
-    dim3 grid(a.L.Cmax256, a.g->n_kv_heads, a.g->batch);
-    if (launch(dense_partial_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
-      return SANTA_ERR_CUDA;
-    if (launch(dense_combine_kernel<T, D>, dim3(a.g->n_heads, a.g->batch), dim3(D), 0, a.st, true, p) !=
+    bool done = false;
+    if constexpr (sizeof(T) == 2) {
+      if (stream_eligible(a.g)) {  // tensor-core streaming flash-decoding kernel
+        constexpr int NW = kDenseWarps, SPW = kDenseSlots;
+        constexpr size_t kStageBytes = 2 * (D / 64) * kDenseStageKeys * 128;
+        const size_t smem = 1024 + (size_t)NW * SPW * (kStageBytes + 16) + (size_t)NW * 8 * kPRow * 2;
+        static size_t configured = 0;
+        if (smem > configured) {
+          if (cudaFuncSetAttribute(dense_stream_kernel<T, D, G, NW, SPW>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return SANTA_ERR_CUDA;
+          configured = smem;
+        }
+        CUtensorMap tk, tv;
+        const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
+                                              : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
+        if (!make_kmap(&tk, a.K, rows, D, a.g->dtype, kDenseStageKeys) ||
+            !make_kmap(&tv, a.V, rows, D, a.g->dtype, kDenseStageKeys))
+          return SANTA_ERR_CUDA;
+        DenseStreamParams dp;
+        dp.q = a.q;
+        dp.kv = p.kv;
+        dp.seqlens = a.seqlens;
+        dp.B = p.B;
+        dp.H = p.H;
+        dp.Hkv = p.Hkv;
+        dp.scale_log2 = p.scale_log2;
+        dp.cstats = p.cstats;
+        dp.opart = p.opart;
+        dp.Cmax = p.Cmax;
+        dp.flags = p.flags;
+        const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
+        const int grid = total < num_sms() ? total : num_sms();
+        if (launch(dense_stream_kernel<T, D, G, NW, SPW>, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv,
+                   dp) != cudaSuccess)
+          return SANTA_ERR_CUDA;
+        done = true;
+      }
+    }
+    if (!done) {
+      dim3 grid(a.L.Cmax256, a.g->n_kv_heads, a.g->batch);
+      if (launch(dense_partial_kernel<T, D, G>, grid, dim3(kScoreThreads), 0, a.st, false, p) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+    }
+    if (launch(dense_combine_kernel<T, D>, dim3(a.g->n_heads, a.g->batch), dim3(256), 0, a.st, true, p) !=
         cudaSuccess)
       return SANTA_ERR_CUDA;
     return SANTA_OK;
@@ -508,6 +628,11 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   a.st = reinterpret_cast<cudaStream_t>(stream);
   a.events = reinterpret_cast<cudaEvent_t const*>(events);
   const int G = g->n_heads / g->n_kv_heads;
+  if (kUseFusedStep && !a.events) {  // measured slower than the PDL pair
+    s = dispatch<RunFused>(g->dtype, g->head_dim, G, a);
+    if (s == SANTA_OK) return last_cuda();
+    if (s != SANTA_ERR_UNSUPPORTED) return s;
+  }
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   return last_cuda();

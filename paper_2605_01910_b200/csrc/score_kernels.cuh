@@ -172,7 +172,7 @@ __device__ __forceinline__ void warp_chunk_epilogue(const float* sS, int L, int 
 
 // ---------------------------------------------------------------------------------------
 // 16 keys x G heads from one swizzled smem stage: rows 16*tile + {g, g+8}.
-template <typename T, int D, int G>
+template <typename T, int D, int G, int BOXB = 8192>
 __device__ __forceinline__ void tile_scores_smem(uint32_t stage_addr, int tile, const uint4 (&qf)[D / 64][2],
                                                  float (&acc)[4]) {
   const int lane = threadIdx.x & 31;
@@ -184,8 +184,8 @@ __device__ __forceinline__ void tile_scores_smem(uint32_t stage_addr, int tile, 
 #pragma unroll
     for (int jj = 0; jj < 2; ++jj) {
       const int c = 2 * tig + jj;
-      a[h][jj][0] = lds128(stage_addr + h * 8192 + r0 * 128 + ((c ^ (r0 & 7)) << 4));
-      a[h][jj][1] = lds128(stage_addr + h * 8192 + r1 * 128 + ((c ^ (r1 & 7)) << 4));
+      a[h][jj][0] = lds128(stage_addr + h * BOXB + r0 * 128 + ((c ^ (r0 & 7)) << 4));
+      a[h][jj][1] = lds128(stage_addr + h * BOXB + r1 * 128 + ((c ^ (r1 & 7)) << 4));
     }
   acc[0] = acc[1] = acc[2] = acc[3] = 0.f;
 #pragma unroll
@@ -263,9 +263,9 @@ struct ChunkWalk {
 // mbarrier.test_wait, issues the next stage for whichever warp has a free slot -- no
 // head-of-line blocking behind a slow warp.
 template <typename T, int D, int G, int NW, int SPW, int kAblate = 0>  // kAblate: tools/microbench_score only
-__global__ void __launch_bounds__(32 * (NW + 1), 1)
-    score_stream_kernel(const __grid_constant__ CUtensorMap tmK, ScoreParams p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
+__device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const ScoreParams& p,
+                                                  unsigned char* smem_raw) {
+  const CUtensorMap& tmK = *tmKp;
   constexpr int NSLOT = NW * SPW;
   constexpr int kBoxBytes = 64 * 128;
   constexpr int kStageBytes = (D / 64) * kBoxBytes;
@@ -449,6 +449,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     __syncwarp();
   }
   pdl_launch_dependents();
+}
+
+template <typename T, int D, int G, int NW, int SPW, int kAblate = 0>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    score_stream_kernel(const __grid_constant__ CUtensorMap tmK, ScoreParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  score_stream_body<T, D, G, NW, SPW, kAblate>(&tmK, p, smem_raw);
 }
 
 // ---------------------------------------------------------------------------------------

@@ -12,8 +12,7 @@
 #include <cstdio>
 #include <vector>
 
-#include "sample_kernels.cuh"
-#include "score_kernels.cuh"
+#include "fused_kernel.cuh"
 
 using namespace santa;
 using bf16 = __nv_bfloat16;
@@ -50,7 +49,7 @@ int main() {
   cudaMalloc(&stash, (size_t)B * H * Cmax * L * 4);
   cudaMalloc(&cstats, (size_t)B * H * Cmax * 8);
   cudaMalloc(&misc, 4096);
-  const int ntrace = B * H * 16;
+  const int ntrace = B * H * 16 + 148 * 8;
   cudaMalloc(&trace, ntrace * 8);
   int nsm;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
@@ -135,6 +134,67 @@ int main() {
            }, 40));
   }
   CL = 1;
+  // fused kernel: one cooperative launch
+  {
+    constexpr int NT = 32 * (NW + 1);
+    const size_t fsm = ssm;
+    auto fk = santa_fused_kernel<bf16, 128, 4, NW, SPW>;
+    cudaFuncSetAttribute(fk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm);
+    auto launch_fused = [&](int r, int cl, bool tr) {
+      SampleParams p = pp(r, tr);
+      p.cluster = cl;
+      unsigned long long* sp_part;
+      static float* split = nullptr;
+      if (!split) cudaMalloc(&split, (size_t)B * H * 8 * 128 * 4);
+      p.split_partial = split;
+      (void)sp_part;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(nsm);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = fsm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, fk, tms[r], sp(r), p);
+    };
+    for (int cl = 1; cl <= 8; cl *= 2)
+      printf("fused (CS=%d)    : %7.2f us\n", cl, timed([&](int i) { launch_fused(i % NR, cl, false); }, 40));
+    std::vector<unsigned long long> h(ntrace);
+    std::vector<std::vector<double>> ph(5);
+    for (int rep = 0; rep < 12; ++rep) {
+      launch_fused(rep % NR, 4, true);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h.data(), trace, ntrace * 8, cudaMemcpyDeviceToHost);
+      if (rep < 2) continue;
+      unsigned long long t0 = ~0ull;
+      for (int c = 0; c < nsm; ++c) t0 = std::min(t0, h[B * H * 16 + c * 8 + 0]);
+      for (int c = 0; c < nsm; ++c)
+        for (int i = 0; i < 5; ++i) ph[i].push_back((double)(h[B * H * 16 + c * 8 + i + 1] - t0));
+    }
+    {
+      std::vector<std::vector<double>> q(6);
+      for (int rep = 0; rep < 10; ++rep) {
+        launch_fused(rep % NR, 4, true);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h.data(), trace, ntrace * 8, cudaMemcpyDeviceToHost);
+        for (int c = 0; c < B * H; ++c)
+          for (int i = 0; i < 6; ++i) q[i].push_back((double)(h[c * 16 + i + 1] - h[c * 16 + i]));
+      }
+      const char* pn[6] = {"thresholds", "pdl wait", "cstats+max", "CDF", "chunk search", "search+gather"};
+      for (int i = 0; i < 6; ++i) {
+        std::sort(q[i].begin(), q[i].end());
+        printf("fused item phase %-14s median %7.0f ns\n", pn[i], q[i][q[i].size() / 2]);
+      }
+    }
+    const char* nm[5] = {"score done", "grid.sync #1", "sample item done", "grid.sync #2", "end"};
+    for (int i = 0; i < 5; ++i) {
+      std::sort(ph[i].begin(), ph[i].end());
+      printf("fused t(%-16s) median %8.0f ns  max %8.0f ns (from first CTA start)\n", nm[i], ph[i][ph[i].size() / 2],
+             ph[i].back());
+    }
+  }
   // phase trace in three settings
   const char* names[7] = {"thresholds (Philox)", "griddepcontrol.wait", "cstats load + max", "fp64 CDF scan+clamp",
                           "chunk search (smem)", "in-chunk search+gather", "reduce + store"};
