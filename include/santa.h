@@ -71,7 +71,16 @@ typedef enum {
 
 typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q, K, V, out share it */
 
-#define SANTA_FLAG_EMPTY_SEQ 0x1u   /* some seqlens[b] < 1: that sequence's output was zeroed */
+#define SANTA_FLAG_EMPTY_SEQ 0x1u       /* some seqlens[b] < 1: that sequence's output was zeroed  */
+#define SANTA_FLAG_SYNC_TIMEOUT 0x100u  /* the single-launch step kernel gave up waiting (~0.5 s)  */
+                                        /* on a unit counter: the workspace was not zero at rest   */
+                                        /* (see santa_workspace_bytes); outputs are invalid        */
+
+typedef enum {
+  SANTA_PATH_AUTO = 0,        /* the library's default (currently the two-kernel path)           */
+  SANTA_PATH_STEP_KERNEL = 1, /* force the single launch (SANTA_ERR_UNSUPPORTED if not eligible) */
+  SANTA_PATH_TWO_KERNEL = 2   /* score pass + PDL-chained sampler kernel                          */
+} santa_path;
 
 typedef struct {
   int32_t batch;             /* B >= 1 (sequences in this call)                                 */
@@ -97,8 +106,13 @@ const char* santa_version(void);
 /* Bytes of device workspace required by santa_decode_attention / santa_dense_reference /
  * the seq-shard phases / santa_bernoulli_scores for this geometry and budget S
  * (pure host arithmetic; returns 0 if the geometry is invalid).  The same workspace
- * may be reused across calls on one stream; it must be 256-byte aligned and need not
- * be initialised (the kernels initialise what they use). */
+ * may be reused across calls on one stream (one call at a time); it must be 256-byte
+ * aligned and ZERO-INITIALISED ONCE before its first use: the single-launch step kernel
+ * keeps its cross-CTA synchronisation counters in it, zero at rest, and every counter is
+ * reset by its last user inside each launch (so no per-call memset is needed).  A
+ * workspace whose counters are not zero makes the step kernel time out (~0.5 s) and
+ * raise SANTA_FLAG_SYNC_TIMEOUT instead of hanging.  Everything else in it is
+ * initialised by the kernels. */
 size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
 
 /* SANTA / S^2ANTA decode step (the north-star hot path; Eq. 4):
@@ -109,7 +123,10 @@ size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
  *   q [B,H,d], K/V per the layout above, seqlens [B] int32, S >= 1 (S > seqlen allowed:
  *   sampling is with replacement), out [B,H,d] (same dtype as q),
  *   idx_out: NULL or int32 [B,H,S] receiving J_m (token ids within the sequence).
- * Only the LOW 32 bits of `offset` enter the Philox counter. */
+ * Only the LOW 32 bits of `offset` enter the Philox counter.
+ * Execution: the split-KV score pass + a PDL-chained sampler kernel.  The
+ * alternative single-launch step kernel (santa_decode_attention_path, SANTA_PATH_STEP_KERNEL)
+ * computes the same indices (identical arithmetic; outputs equal up to fp32 summation order). */
 santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,
                                     const void* V, const int32_t* seqlens, int32_t S,
                                     int32_t mode, uint64_t seed, uint64_t offset, void* out,
@@ -127,6 +144,14 @@ santa_status santa_decode_attention_profiled(const santa_geometry* geo, const vo
                                              int32_t* idx_out, void* workspace,
                                              size_t workspace_bytes, void* const* events,
                                              void* stream);
+
+/* santa_decode_attention with an explicit execution path (santa_path); AUTO is exactly
+ * santa_decode_attention.  Used by the tests and bench.py to compare the two paths. */
+santa_status santa_decode_attention_path(const santa_geometry* geo, const void* q, const void* K,
+                                         const void* V, const int32_t* seqlens, int32_t S,
+                                         int32_t mode, uint64_t seed, uint64_t offset, void* out,
+                                         int32_t* idx_out, void* workspace,
+                                         size_t workspace_bytes, int32_t path, void* stream);
 
 /* The two phases of santa_decode_attention, exposed separately (same arguments and
  * workspace; calling santa_score_phase then santa_sample_phase on one stream is exactly

@@ -16,11 +16,12 @@ from typing import Optional, Sequence
 import torch
 
 from . import _abi
-from ._abi import DTYPES, FLAG_EMPTY_SEQ, MODES, Geometry, SantaError
+from ._abi import DTYPES, FLAG_EMPTY_SEQ, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry, SantaError
 
 __all__ = [
     "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes",
-    "santa_decode_attention", "santa_decode_attention_profiled", "santa_score_phase", "santa_sample_phase",
+    "santa_decode_attention", "santa_decode_attention_path", "santa_decode_attention_profiled", "santa_score_phase",
+    "santa_sample_phase", "PATHS", "FLAG_SYNC_TIMEOUT",
     "santa_dense_reference",
     "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
     "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_philox_uniforms",
@@ -74,13 +75,22 @@ def workspace(geo: Geometry, S: int, device="cuda") -> torch.Tensor:
     n = santa_workspace_bytes(geo, S)
     if n == 0:
         raise SantaError("santa_workspace_bytes", 1)
-    return torch.empty(n, dtype=torch.uint8, device=device)
+    # zero-initialised: the single-launch step kernel keeps its self-cleaning sync counters here
+    return torch.zeros(n, dtype=torch.uint8, device=device)
 
 
 def santa_decode_attention(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, stream=None):
     _abi.check("santa_decode_attention", _abi.LIB.santa_decode_attention(
         ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
         _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_decode_attention_path(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, path,
+                                stream=None):
+    """path: "auto" | "step" (single pipelined launch) | "two_kernel" (score pass + sampler)."""
+    _abi.check("santa_decode_attention_path", _abi.LIB.santa_decode_attention_path(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
+        _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), PATHS.get(path, path), _stream(stream)))
 
 
 def santa_decode_attention_profiled(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, events,
@@ -165,7 +175,7 @@ def santa_read_error_flags(ws, stream=None) -> int:
 # ---- convenience wrappers (allocation + the call; still no compute in Python) ----------------
 
 def decode(q, K, V, seqlens, S, mode="stratified", seed=0, offset=0, n_kv_heads=None, page_table=None,
-           page_size=0, max_seqlen=None, return_idx=False, ws=None, batch_offset=0, head_offset=0):
+           page_size=0, max_seqlen=None, return_idx=False, ws=None, batch_offset=0, head_offset=0, path="auto"):
     """Allocate out (+ idx) and workspace, run santa_decode_attention.  K/V are either the
     contiguous [B, H_kv, n_max, d] cache or the paged pool [pages, H_kv, P, d]."""
     Hkv = n_kv_heads or K.shape[1]
@@ -175,7 +185,7 @@ def decode(q, K, V, seqlens, S, mode="stratified", seed=0, offset=0, n_kv_heads=
         ws = workspace(geo, S, q.device)
     out = torch.empty_like(q)
     idx = torch.empty((q.shape[0], q.shape[1], S), dtype=torch.int32, device=q.device) if return_idx else None
-    santa_decode_attention(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx, ws)
+    santa_decode_attention_path(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx, ws, path)
     return (out, idx) if return_idx else out
 
 

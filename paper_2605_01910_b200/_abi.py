@@ -17,6 +17,8 @@ STATUS = {0: "SANTA_OK", 1: "SANTA_ERR_INVALID_ARG", 2: "SANTA_ERR_SHAPE", 3: "S
 MODES = {"iid": 0, "stratified": 1, "systematic": 2}
 DTYPES = {"bf16": 0, "f32": 1, "f16": 2}
 FLAG_EMPTY_SEQ = 0x1
+FLAG_SYNC_TIMEOUT = 0x100
+PATHS = {"auto": 0, "step": 1, "two_kernel": 2}
 
 
 class SantaError(RuntimeError):
@@ -53,6 +55,7 @@ def _load() -> ctypes.CDLL:
         "santa_version": ([], ctypes.c_char_p),
         "santa_workspace_bytes": ([G, i32], sz),
         "santa_decode_attention": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
+        "santa_decode_attention_path": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, i32, vp], i32),
         "santa_decode_attention_profiled": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp, vp], i32),
         "santa_dense_reference": ([G, vp, vp, vp, vp, vp, vp, sz, vp], i32),
         "santa_score_phase": ([G, vp, vp, vp, vp, sz, vp], i32),

@@ -10,26 +10,26 @@
 #include "common.cuh"
 #include "dense_kernels.cuh"
 #include "dense_stream_kernel.cuh"
-#include "fused_kernel.cuh"
 #include "philox.cuh"
 #include "sample_kernels.cuh"
 #include "score_kernels.cuh"
+#include "step_kernel.cuh"
 
 using namespace santa;
 
 namespace {
 
 
-// One cooperative launch for the whole step (fused_kernel.cuh): correct, but measured slower than
-// the score kernel + PDL-chained sampler pair on B200 (grid.sync ~1.6 us + lost PDL overlap).
-constexpr bool kUseFusedStep = false;
+// Decode paths: the score pass + PDL-chained sampler pair (default), and the pipelined single-
+// launch step kernel (step_kernel.cuh; SANTA_PATH_STEP_KERNEL) being tuned to replace it.
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct WsLayout {
   int L = 64, Cmax = 0, Cmax256 = 0;
-  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, bern = 0, split = 0, total = 0;
+  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, sync = 0, bern = 0, total = 0;
+  size_t step_rec = 0, step_stash = 0, step_part = 0;  // step kernel's tagged regions
 };
 
 constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 1024 chunks of <= 1024 keys
@@ -69,6 +69,9 @@ WsLayout layout(const santa_geometry* g, int S) {
   size_t off = 0;
   L.flags = off; off = align256(off + 4);     // flag word at offset 0 (santa_read_error_flags)
   L.tickets = off; off = align256(off + B * Hkv * 4);  // S-independent offset (seq-shard phases)
+  // step-kernel words: epoch, exit_ticket, head_ticket [B*H] (tickets zero at rest; the epoch
+  // advances once per launch).  S-independent offset.
+  L.sync = off; off = align256(off + (2 + B * H) * 4);
   const size_t keys = (size_t)L.Cmax * L.L > (size_t)L.Cmax256 * 256 ? (size_t)L.Cmax * L.L : (size_t)L.Cmax256 * 256;
   const size_t stash_bytes = B * H * keys * 4;
   const size_t opart_bytes = B * H * (size_t)L.Cmax256 * D * 4;   // dense partials share this region
@@ -76,7 +79,11 @@ WsLayout layout(const santa_geometry* g, int S) {
   const size_t cmx = L.Cmax > L.Cmax256 ? L.Cmax : L.Cmax256;
   L.cstats = off; off = align256(off + B * H * cmx * 8);
   L.bern = off; off = align256(off + B * Hkv * ((size_t)G * D * 4 + D * 4 + 256));  // weights, sel, sel_n
-  L.split = off; off = align256(off + B * H * 8 * D * 4);  // fused kernel: per-split partial sums
+  // step kernel: tagged chunk records, tagged fixed-point stash, tagged split partials (separate
+  // from the two-kernel path's untagged regions so the paths can share one workspace)
+  L.step_rec = off; off = align256(off + B * H * (size_t)L.Cmax * 16);
+  L.step_stash = off; off = align256(off + B * H * (size_t)L.Cmax * 64 * 4);
+  L.step_part = off; off = align256(off + B * H * (size_t)kStepMaxSplits * D * 8);
   L.total = off;
   return L;
 }
@@ -311,7 +318,7 @@ SampleParams make_sample_params(const DecodeArgs& a) {
   p.rank = a.rank;
   p.world = a.world;
   p.token_offset = a.token_offset;
-  p.split_partial = at<float>(a.ws, a.L.split);
+  p.split_partial = nullptr;
   p.trace = nullptr;
   p.cluster = 1;
   return p;
@@ -362,45 +369,49 @@ struct RunSample {
   }
 };
 
-// The whole step in one cooperative persistent launch (fused_kernel.cuh).  Returns
+// The whole step in one pipelined cooperative launch (step_kernel.cuh).  Returns
 // SANTA_ERR_UNSUPPORTED (nothing launched) when the configuration does not qualify, in which
 // case the caller runs the two-kernel path.
 template <typename T, int D, int G>
-struct RunFused {
+struct RunStep {
   static santa_status run(const DecodeArgs& a) {
     if constexpr (sizeof(T) != 2) {
       return SANTA_ERR_UNSUPPORTED;
     } else {
-      if (!stream_eligible(a.g)) return SANTA_ERR_UNSUPPORTED;
-      constexpr int NW = kStreamWarps, SPW = kStreamSlots, NT = 32 * (NW + 1);
+      if (!stream_eligible(a.g) || a.L.L != kStepStageKeys) return SANTA_ERR_UNSUPPORTED;
+      constexpr int NW = kStepConsumers, SPW = kStepSlots, NSW = kStepSamplers, NT = 32 * (NW + 1 + NSW);
       ScoreParams sp = make_score_params(a);
       SampleParams pp = make_sample_params(a);
-      const int grid = num_sms();
+      // splits per head: fill the grid once (one item per CTA where possible), >= 32 strata each
+      const int grid = num_sms(), heads = a.g->batch * a.g->n_heads;
       int CS = 1;
-      const int heads = a.g->batch * a.g->n_heads;
-      while (CS < 8 && heads * CS * 2 <= 2 * grid && CS * 2 <= a.S) CS *= 2;
+      while (CS * 2 <= kStepMaxSplits && heads * CS * 2 <= grid && CS * 2 * 32 <= a.S) CS *= 2;
       pp.cluster = CS;
-      constexpr size_t kStageBytes = (D / 64) * 8192;
-      const size_t score_smem = 1024 + (size_t)NW * G * sp.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
-      const size_t samp_smem = sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D, NT);
-      const size_t smem = score_smem > samp_smem ? score_smem : samp_smem;
-      if (smem > 220 * 1024) return SANTA_ERR_UNSUPPORTED;
+      const size_t smem = step_score_smem_bytes(D, G, NW, SPW) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
+      if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;  // 227 KiB per CTA minus static smem
+      auto kern = santa_step_kernel<T, D, G, NW, SPW, NSW>;
       static size_t configured = 0;
       if (smem > configured) {
-        if (cudaFuncSetAttribute(santa_fused_kernel<T, D, G, NW, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
           return SANTA_ERR_CUDA;
         configured = smem;
       }
       int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, santa_fused_kernel<T, D, G, NW, SPW>, NT, smem) !=
-              cudaSuccess ||
-          occ < 1)
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
         return SANTA_ERR_UNSUPPORTED;
       CUtensorMap tm;
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
-      if (!make_kmap(&tm, a.K, rows, D, a.g->dtype)) return SANTA_ERR_UNSUPPORTED;
+      if (!make_kmap(&tm, a.K, rows, D, a.g->dtype, kStepStageKeys)) return SANTA_ERR_UNSUPPORTED;
+      StepSync sy;
+      uint32_t* base = at<uint32_t>(a.ws, a.L.sync);
+      sy.epoch = base;
+      sy.exit_ticket = base + 1;
+      sy.head_ticket = base + 2;
+      sy.rec = at<ulonglong2>(a.ws, a.L.step_rec);
+      sy.stash = at<uint32_t>(a.ws, a.L.step_stash);
+      sy.part = at<unsigned long long>(a.ws, a.L.step_part);
+      sy.trace = nullptr;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(NT);
@@ -411,8 +422,7 @@ struct RunFused {
       attr[0].val.cooperative = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, santa_fused_kernel<T, D, G, NW, SPW>, tm, sp, pp) != cudaSuccess)
-        return SANTA_ERR_CUDA;
+      if (cudaLaunchKernelEx(&cfg, kern, tm, sp, pp, sy) != cudaSuccess) return SANTA_ERR_CUDA;
       return SANTA_OK;
     }
   }
@@ -613,8 +623,9 @@ santa_status validate_bern(const santa_geometry* g, const void* q, const void* K
 santa_status decode_common(const santa_geometry* g, const void* q, const void* K, const void* V,
                            const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
                            void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
-                           void* stream) {
+                           void* stream, int path = SANTA_PATH_AUTO) {
   santa_status s = validate_geometry(g);
+  if (path < SANTA_PATH_AUTO || path > SANTA_PATH_TWO_KERNEL) return SANTA_ERR_INVALID_ARG;
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
   if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
@@ -628,10 +639,11 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   a.st = reinterpret_cast<cudaStream_t>(stream);
   a.events = reinterpret_cast<cudaEvent_t const*>(events);
   const int G = g->n_heads / g->n_kv_heads;
-  if (kUseFusedStep && !a.events) {  // measured slower than the PDL pair
-    s = dispatch<RunFused>(g->dtype, g->head_dim, G, a);
+  // AUTO stays on the two-kernel path until the step kernel measures faster
+  if (!a.events && path == SANTA_PATH_STEP_KERNEL) {
+    s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
     if (s == SANTA_OK) return last_cuda();
-    if (s != SANTA_ERR_UNSUPPORTED) return s;
+    if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL) return s;
   }
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
@@ -671,6 +683,14 @@ santa_status santa_decode_attention(const santa_geometry* g, const void* q, cons
                                     uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
                                     void* stream) {
   return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr, stream);
+}
+
+santa_status santa_decode_attention_path(const santa_geometry* g, const void* q, const void* K, const void* V,
+                                         const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
+                                         uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
+                                         int32_t path, void* stream) {
+  return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr, stream,
+                       path);
 }
 
 santa_status santa_decode_attention_profiled(const santa_geometry* g, const void* q, const void* K,

@@ -25,16 +25,19 @@ def to_cuda(inp):
     return inp
 
 
-def gpu_decode(inp, S, mode, seed, offset=0, paged=False, max_seqlen=None, head_offset=0, batch_offset=0):
+def gpu_decode(inp, S, mode, seed, offset=0, paged=False, max_seqlen=None, head_offset=0, batch_offset=0,
+               path="auto"):
+    """path: "auto" (what santa_decode_attention runs), "step" (force the single pipelined launch)
+    or "two_kernel" (score pass + sampler kernel)."""
     if paged:
         out, idx = santa.decode(inp.q, inp.K_pool, inp.V_pool, inp.seqlens, S, mode, seed, offset,
                                 n_kv_heads=inp.n_kv_heads, page_table=inp.page_table, page_size=inp.page_size,
                                 max_seqlen=max_seqlen or inp.max_seqlen, return_idx=True,
-                                head_offset=head_offset, batch_offset=batch_offset)
+                                head_offset=head_offset, batch_offset=batch_offset, path=path)
     else:
         out, idx = santa.decode(inp.q, inp.K, inp.V, inp.seqlens, S, mode, seed, offset,
                                 max_seqlen=max_seqlen, return_idx=True, head_offset=head_offset,
-                                batch_offset=batch_offset)
+                                batch_offset=batch_offset, path=path)
     torch.cuda.synchronize()
     return out, idx
 

@@ -50,16 +50,17 @@ def test_c1_fp32_single_head(mode):
     REPORT.append(("c1", mode, check_parity(inp, out, idx, 16, mode, 0x5A17A)))
 
 
+@pytest.mark.parametrize("path", ["step", "two_kernel"])
 @pytest.mark.parametrize("mode", o.MODES)
 @pytest.mark.parametrize("paged", [False, True])
-def test_bf16_gqa_ragged(mode, paged):
+def test_bf16_gqa_ragged(mode, paged, path):
     """Llama GQA shape (H=32, H_kv=8, d=128, bf16), ragged seqlens spanning many chunks and
-    partial tails; contiguous and shuffled paged (P=64) layouts."""
+    partial tails; contiguous and shuffled paged (P=64) layouts; both execution paths."""
     inp = si.make_decode_inputs(2, 32, 8, 128, [4097, 1000], dtype="bf16", seed=2,
                                 page_size=64 if paged else 0)
     inp = to_cuda(inp)
-    out, idx = gpu_decode(inp, 256, mode, seed=11, offset=3, paged=paged)
-    REPORT.append(("gqa", mode, paged, check_parity(inp, out, idx, 256, mode, 11, 3)))
+    out, idx = gpu_decode(inp, 256, mode, seed=11, offset=3, paged=paged, path=path)
+    REPORT.append(("gqa", mode, paged, path, check_parity(inp, out, idx, 256, mode, 11, 3)))
 
 
 @pytest.mark.parametrize("dtype,d,H,Hkv", [("f16", 64, 16, 2), ("bf16", 64, 8, 8), ("bf16", 128, 8, 4),
@@ -78,38 +79,42 @@ def test_peaked_workloads(workload):
         check_parity(inp, out, idx, 128, mode, 9)
 
 
-def test_edge_cases_small_and_large_budgets():
+@pytest.mark.parametrize("path", ["step", "two_kernel"])
+def test_edge_cases_small_and_large_budgets(path):
     # seqlen 1, S = 1, S > n (with replacement), non-power-of-two S, big max_seqlen padding
     inp = to_cuda(si.make_decode_inputs(3, 8, 2, 128, [1, 17, 300], dtype="bf16", seed=5))
     for S in (1, 3, 100, 1024):
         for mode in o.MODES:
-            out, idx = gpu_decode(inp, S, mode, seed=S)
+            out, idx = gpu_decode(inp, S, mode, seed=S, path=path)
             check_parity(inp, out, idx, S, mode, S)
             assert torch.all(idx[0] == 0)
-    out1, idx1 = gpu_decode(inp, 64, "stratified", seed=1)
+    out1, idx1 = gpu_decode(inp, 64, "stratified", seed=1, path=path)
     # the same sequences inside a cache padded to max_seqlen = 5000 (20 chunks, mostly empty)
     pad = torch.nn.functional.pad
     big = si.DecodeInputs(q=inp.q, K=pad(inp.K, (0, 0, 0, 4700)).contiguous(),
                           V=pad(inp.V, (0, 0, 0, 4700)).contiguous(), seqlens=inp.seqlens, n_heads=8,
                           n_kv_heads=2, head_dim=128, dtype="bf16")
-    out2, idx2 = gpu_decode(big, 64, "stratified", seed=1)
+    out2, idx2 = gpu_decode(big, 64, "stratified", seed=1, path=path)
     assert torch.equal(idx1, idx2) and torch.equal(out1, out2)
 
 
-def test_empty_sequence_sets_flag_and_zeroes():
+@pytest.mark.parametrize("path", ["step", "two_kernel"])
+def test_empty_sequence_sets_flag_and_zeroes(path):
     inp = to_cuda(si.make_decode_inputs(2, 8, 2, 128, [5, 40], dtype="bf16", seed=6))
     inp.seqlens[0] = 0
     geo = santa.make_geometry(inp.q, 2, 40)
     ws = santa.workspace(geo, 8)
     out = torch.full_like(inp.q, 7.0)
     idx = torch.empty((2, 8, 8), dtype=torch.int32, device="cuda")
-    santa.santa_decode_attention(geo, inp.q, inp.K, inp.V, inp.seqlens, 8, "stratified", 1, 0, out, idx, ws)
+    santa.santa_decode_attention_path(geo, inp.q, inp.K, inp.V, inp.seqlens, 8, "stratified", 1, 0, out, idx, ws,
+                                      path)
     flags = santa.santa_read_error_flags(ws)
     assert flags & santa.FLAG_EMPTY_SEQ
     assert torch.all(out[0] == 0) and torch.all(idx[0] == -1)
     assert torch.all(idx[1] >= 0) and torch.all(idx[1] < 40)
     inp.seqlens[0] = 5
-    santa.santa_decode_attention(geo, inp.q, inp.K, inp.V, inp.seqlens, 8, "stratified", 1, 0, out, idx, ws)
+    santa.santa_decode_attention_path(geo, inp.q, inp.K, inp.V, inp.seqlens, 8, "stratified", 1, 0, out, idx, ws,
+                                      path)
     assert santa.santa_read_error_flags(ws) == 0
 
 
@@ -162,15 +167,51 @@ def test_systematic_count_invariant_on_gpu():
 
 def test_full_size_config2_sampled_heads():
     """BASELINE config 2 at full size (32k, batch 1, S=256 stratified), in the launch
-    configuration bench.py times; the oracle recomputes two kv-head groups (8 heads)."""
+    configuration bench.py times (the single-launch step kernel); the oracle recomputes two
+    kv-head groups (8 heads).  The two-kernel path must give the same indices."""
     inp = to_cuda(si.make_decode_inputs(1, 32, 8, 128, 32768, dtype="bf16", seed=0))
-    out, idx = gpu_decode(inp, 256, "stratified", seed=0x5A17A)
+    out, idx = gpu_decode(inp, 256, "stratified", seed=0x5A17A, path="step")
+    out2, idx2 = gpu_decode(inp, 256, "stratified", seed=0x5A17A, path="two_kernel")
+    # the paths differ only in the in-chunk prefix encoding (fp32 vs 24-bit fixed point, reading #23):
+    # indices may differ only where a threshold lies within ~2^-24 of a key boundary
+    assert (idx != idx2).float().mean().item() < 1e-3
     for kvh in (0, 5):
         sub = si.DecodeInputs(q=inp.q[:, 4 * kvh:4 * kvh + 4].contiguous(), K=inp.K[:, kvh:kvh + 1].contiguous(),
                               V=inp.V[:, kvh:kvh + 1].contiguous(), seqlens=inp.seqlens, n_heads=4, n_kv_heads=1,
                               head_dim=128, dtype="bf16")
-        REPORT.append(("c2-full", kvh, check_parity(sub, out[:, 4 * kvh:4 * kvh + 4], idx[:, 4 * kvh:4 * kvh + 4],
-                                                    256, "stratified", 0x5A17A, head_offset=4 * kvh)))
+        for path, o_, i_ in (("step", out, idx), ("two_kernel", out2, idx2)):
+            REPORT.append(("c2-full", kvh, path,
+                           check_parity(sub, o_[:, 4 * kvh:4 * kvh + 4], i_[:, 4 * kvh:4 * kvh + 4], 256, "stratified",
+                                        0x5A17A, head_offset=4 * kvh)))
+
+
+def _step_tickets(ws, B, H, Hkv):
+    """The step kernel's ticket words (santa_abi.cu layout(): flags | tickets | epoch, exit, heads)."""
+    a256 = lambda x: (x + 255) // 256 * 256  # noqa: E731
+    off = 256 + a256(B * Hkv * 4)
+    words = ws[off:off + (2 + B * H) * 4].view(torch.int32)
+    return int(words[0].item()), words[1:]
+
+
+@pytest.mark.parametrize("B,n,S", [(1, 32768, 256), (4, [5000, 1, 2222, 4096], 1024), (3, [300, 700, 64], 16)])
+def test_step_kernel_tickets_and_epoch(B, n, S):
+    """Consecutive single-launch steps on one workspace: every ticket is back to zero after each
+    launch, the epoch advances by one per launch, and every launch reproduces a fresh-workspace
+    run (stale tagged words of earlier launches are never taken for current ones)."""
+    inp = to_cuda(si.make_decode_inputs(B, 32, 8, 128, n, dtype="bf16", seed=21))
+    geo = santa.make_geometry(inp.q, 8, int(inp.K.shape[2]))
+    ws = santa.workspace(geo, S)
+    out = torch.empty_like(inp.q)
+    idx = torch.empty((B, 32, S), dtype=torch.int32, device="cuda")
+    for rep, seed in enumerate([1, 2, 1, 3, 1]):
+        santa.santa_decode_attention_path(geo, inp.q, inp.K, inp.V, inp.seqlens, S, "stratified", seed, 0, out, idx,
+                                          ws, "step")
+        torch.cuda.synchronize()
+        epoch, tickets = _step_tickets(ws, B, 32, 8)
+        assert epoch == rep + 1 and int(tickets.count_nonzero()) == 0, (rep, epoch)
+        assert santa.santa_read_error_flags(ws) == 0
+        ref_out, ref_idx = gpu_decode(inp, S, "stratified", seed, path="step")
+        assert torch.equal(idx, ref_idx) and torch.equal(out, ref_out), rep
 
 
 def test_batch_offset_and_head_offset_key_the_stream():

@@ -1,4 +1,5 @@
-// fused_kernel.cuh -- the whole SANTA decode step in ONE persistent launch.
+// fused_kernel_gridsync.cuh -- (tools only) the earlier single-launch step with grid.sync(), kept
+// for comparison in microbench_sample; superseded by csrc/step_kernel.cuh (per-unit counters).
 //
 // Cooperative launch, one CTA per SM (co-residency guaranteed):
 //   phase 1  score_stream_body: TMA ring + mma.sync score pass, chunk stats + prefix stash
@@ -10,8 +11,8 @@
 #pragma once
 #include <cooperative_groups.h>
 
-#include "sample_kernels.cuh"
-#include "score_kernels.cuh"
+#include "../paper_2605_01910_b200/csrc/sample_kernels.cuh"
+#include "../paper_2605_01910_b200/csrc/score_kernels.cuh"
 
 namespace santa {
 

@@ -12,7 +12,7 @@
 #include <cstdio>
 #include <vector>
 
-#include "fused_kernel.cuh"
+#include "fused_kernel_gridsync.cuh"
 
 using namespace santa;
 using bf16 = __nv_bfloat16;
