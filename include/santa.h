@@ -77,7 +77,7 @@ typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q,
                                         /* (see santa_workspace_bytes); outputs are invalid        */
 
 typedef enum {
-  SANTA_PATH_AUTO = 0,        /* the library's default (currently the two-kernel path)           */
+  SANTA_PATH_AUTO = 0,        /* the step kernel when eligible, else the two-kernel path          */
   SANTA_PATH_STEP_KERNEL = 1, /* force the single launch (SANTA_ERR_UNSUPPORTED if not eligible) */
   SANTA_PATH_TWO_KERNEL = 2   /* score pass + PDL-chained sampler kernel                          */
 } santa_path;
@@ -124,9 +124,13 @@ size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
  *   sampling is with replacement), out [B,H,d] (same dtype as q),
  *   idx_out: NULL or int32 [B,H,S] receiving J_m (token ids within the sequence).
  * Only the LOW 32 bits of `offset` enter the Philox counter.
- * Execution: the split-KV score pass + a PDL-chained sampler kernel.  The
- * alternative single-launch step kernel (santa_decode_attention_path, SANTA_PATH_STEP_KERNEL)
- * computes the same indices (identical arithmetic; outputs equal up to fp32 summation order). */
+ * Execution: for bf16/fp16 caches (contiguous, or pages of a multiple of 64
+ * tokens) and max_seqlen <= 65536 the whole step is ONE cooperative persistent launch (the step
+ * kernel: interleaved TMA score stream; each (b, kv-head) unit is sampled as soon as its chunks are
+ * scored, chunk results published as tagged words -- no fences); otherwise the split-KV score pass
+ * + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
+ * in-chunk prefixes are fp32 (two-kernel) vs 24-bit fixed point (step kernel, DESIGN.md reading
+ * #23), so an index may differ only where a threshold lies within ~2^-24 of a key boundary. */
 santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,
                                     const void* V, const int32_t* seqlens, int32_t S,
                                     int32_t mode, uint64_t seed, uint64_t offset, void* out,

@@ -20,8 +20,9 @@ using namespace santa;
 namespace {
 
 
-// Decode paths: the score pass + PDL-chained sampler pair (default), and the pipelined single-
-// launch step kernel (step_kernel.cuh; SANTA_PATH_STEP_KERNEL) being tuned to replace it.
+// Decode paths: the pipelined single-launch step kernel (step_kernel.cuh; default when eligible)
+// and the score pass + PDL-chained sampler pair (fp32 caches, page sizes not a multiple of 64,
+// contexts > 64k, profiling, and the sequence-sharded phases).
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -382,10 +383,13 @@ struct RunStep {
       constexpr int NW = kStepConsumers, SPW = kStepSlots, NSW = kStepSamplers, NT = 32 * (NW + 1 + NSW);
       ScoreParams sp = make_score_params(a);
       SampleParams pp = make_sample_params(a);
-      // splits per head: fill the grid once (one item per CTA where possible), >= 32 strata each
+      // splits per head: aim at one sampler round (<= 64 strata) per item, so the exposed tail (the
+      // last unit's items) is one gather round, but keep the total at <= 4 items per CTA: every item
+      // repeats the chunk-CDF combine, and at large batch the sampler work must stay hidden under
+      // the stream (config 3, S = 512: 8192 items -> 661 us vs 1024 items -> see DESIGN.md sec. 5)
       const int grid = num_sms(), heads = a.g->batch * a.g->n_heads;
       int CS = 1;
-      while (CS * 2 <= kStepMaxSplits && heads * CS * 2 <= grid && CS * 2 * 32 <= a.S) CS *= 2;
+      while (CS * 2 <= kStepMaxSplits && CS * 64 < a.S && heads * CS * 2 <= 4 * grid) CS *= 2;
       pp.cluster = CS;
       const size_t smem = step_score_smem_bytes(D, G, NW, SPW) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
       if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;  // 227 KiB per CTA minus static smem
@@ -396,9 +400,13 @@ struct RunStep {
           return SANTA_ERR_CUDA;
         configured = smem;
       }
-      int occ = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
-        return SANTA_ERR_UNSUPPORTED;
+      static size_t occ_checked = 0;  // host-side per-call cost matters at ~25 us per step: query once per size
+      if (smem > occ_checked) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
+          return SANTA_ERR_UNSUPPORTED;
+        occ_checked = smem;
+      }
       CUtensorMap tm;
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
@@ -639,8 +647,9 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   a.st = reinterpret_cast<cudaStream_t>(stream);
   a.events = reinterpret_cast<cudaEvent_t const*>(events);
   const int G = g->n_heads / g->n_kv_heads;
-  // AUTO stays on the two-kernel path until the step kernel measures faster
-  if (!a.events && path == SANTA_PATH_STEP_KERNEL) {
+  // AUTO = the single-launch step kernel when eligible (measured >= the two-kernel path at every
+  // batch size of config 3, tools/path_sweep.py)
+  if (!a.events && path != SANTA_PATH_TWO_KERNEL) {
     s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
     if (s == SANTA_OK) return last_cuda();
     if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL) return s;

@@ -228,36 +228,49 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
     return sPart;
   }
   const ulonglong2* rec = sy.rec + bh * p.Cmax;
-  // ---- wait: every thread loads its chunk records and re-polls the stale ones (below) ----
-  if (tid == 0 && tslot >= 0) STEP_TRACE(tslot + 1);
+  // ---- wait: one thread polls the unit's last chunk (it is scored last) with a short back-off, so
+  // the ~10^4 waiting sampler threads of a step do not flood L2 while the stream runs ----
+  if (tid == 0) {
+    const unsigned long long t0 = gtimer();
+    while (!rec_valid(ld_strong_v2_u64(rec + nC - 1), tag32)) {
+      if (poll_expired(t0)) {
+        atomicOr(p.flags, SANTA_FLAG_SYNC_TIMEOUT);
+        break;
+      }
+      __nanosleep(64);
+    }
+    if (tslot >= 0) STEP_TRACE(tslot + 1);
+  }
+  group_bar();
 
-  // ---- a3: chunk records -> fp64 chunk CDF (reading #5 clamp) ----
-  const int per = (nC + NT - 1) / NT;
-  const int c0 = min(tid * per, nC), c1 = min(c0 + per, nC);
+  // ---- a3: chunk records -> fp64 chunk CDF (reading #5 clamp), values kept in registers ----
+  constexpr int kCPT = 8;                     // chunks per thread (Cmax <= 1024 on this path)
+  const int per = (nC + NT - 1) / NT;         // <= kCPT
+  const int c0 = min(tid * per, nC);
+  const int nmine = min(per, nC - c0);
+  float mreg[kCPT], lreg[kCPT];
   float mloc = -INFINITY;
   {
-    // issue up to kRB record loads at once (one L2 round trip), then re-poll only stale ones
-    constexpr int kRB = 8;
+    ulonglong2 r[kCPT];
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i)
+      if (i < nmine) r[i] = ld_strong_v2_u64(rec + c0 + i);  // one round trip for all of them
     const unsigned long long t0 = gtimer();
-    for (int cb = c0; cb < c1; cb += kRB) {
-      ulonglong2 r[kRB];
 #pragma unroll
-      for (int i = 0; i < kRB; ++i)
-        if (cb + i < c1) r[i] = ld_strong_v2_u64(rec + cb + i);
-#pragma unroll
-      for (int i = 0; i < kRB; ++i) {
-        if (cb + i >= c1) break;
-        while (!rec_valid(r[i], tag32)) {
+    for (int i = 0; i < kCPT; ++i) {
+      mreg[i] = -INFINITY;
+      lreg[i] = 0.f;
+      if (i < nmine) {
+        while (!rec_valid(r[i], tag32)) {  // rare: a record not yet visible
           if (poll_expired(t0)) {
             atomicOr(p.flags, SANTA_FLAG_SYNC_TIMEOUT);
             break;
           }
-          r[i] = ld_strong_v2_u64(rec + cb + i);
+          r[i] = ld_strong_v2_u64(rec + c0 + i);
         }
-        const float mc = __uint_as_float((uint32_t)r[i].x);
-        sF[cb + i] = (double)mc;                              // m_c (temporarily)
-        sR[cb + i] = (double)__uint_as_float((uint32_t)r[i].y);  // l_c (temporarily)
-        mloc = fmaxf(mloc, mc);
+        mreg[i] = __uint_as_float((uint32_t)r[i].x);
+        lreg[i] = __uint_as_float((uint32_t)r[i].y);
+        mloc = fmaxf(mloc, mreg[i]);
       }
     }
   }
@@ -270,14 +283,14 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   for (int w = 1; w < NW; ++w) mstar = fmaxf(mstar, gred_f[w]);
   // W_c = 2^(m_c - m*) l_c: the power in fp32 (ex2.approx, 2 ulp) -- the fp32 scores already carry
   // errors of that order -- and everything downstream (products, sums, CDF) in fp64
+  double wv[kCPT];
   double part = 0.0;
   int lastpos = -1;
-  for (int c = c0; c < c1; ++c) {
-    const double l = sR[c];
-    const double w = l > 0.0 ? (double)ex2((float)sF[c] - mstar) * l : 0.0;
-    sR[c] = w;  // W_c
-    part += w;
-    if (w > 0.0) lastpos = c;
+#pragma unroll
+  for (int i = 0; i < kCPT; ++i) {
+    wv[i] = lreg[i] > 0.f ? (double)ex2(mreg[i] - mstar) * (double)lreg[i] : 0.0;
+    part += wv[i];
+    if (wv[i] > 0.0) lastpos = c0 + i;
   }
   {
     const double incl = warp_incl_scan_d(part, lane);
@@ -298,9 +311,13 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
     }
     double run = off + incl - part;
     const double invZ = 1.0 / Z;
-    for (int c = c0; c < c1; ++c) {
-      run += sR[c];
-      sF[c] = c >= lpos ? 1.0 : run * invZ;
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i) {
+      if (i < nmine) {
+        run += wv[i];
+        sF[c0 + i] = c0 + i >= lpos ? 1.0 : run * invZ;
+        sR[c0 + i] = wv[i];
+      }
     }
     if (tid == 0) gZ = Z;
   }
