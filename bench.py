@@ -70,8 +70,8 @@ def load_peaks():
 
 
 def load_traffic():
-    """dram bytes per launch of the score kernel from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "score_kernel_ncu.json")
+    """dram bytes per launch of the dominant (step) kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "dominant_kernel_ncu.json")
     if os.path.exists(p):
         try:
             return json.load(open(p)).get("dram_bytes_per_launch")
