@@ -190,7 +190,7 @@ __device__ __forceinline__ void warp_chunk_epilogue_ll(const float* sS, int n_va
 // (reading #23).  Returns the partial sum (not yet x 1/S) in sPart[D].
 template <typename T, int D, int G>
 __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, int b, int h, int rank, int CS,
-                                   unsigned char* smem, int tslot, uint32_t tag32, uint32_t tag8) {
+                                   unsigned char* smem, int tslot, uint32_t tag32, uint32_t tag8, bool dry) {
   constexpr int NT = kStepSamplers * 32, NW = kStepSamplers, NHW = NT / 16;
   const int tid = threadIdx.x - (blockDim.x - NT);  // 0..NT-1 within the group
   const int lane = tid & 31, wg = tid >> 5;
@@ -222,7 +222,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   if (tid == 0 && tslot >= 0) STEP_TRACE(tslot + 0);
   if (nC == 0) {  // empty distribution: zero partial (the flag was set at kernel start)
     for (int d = tid; d < D; d += NT) sPart[d] = 0.f;
-    if (p.idx_out)
+    if (p.idx_out && !dry)
       for (int i = tid; i < Sl; i += NT) p.idx_out[bh * S + m_lo + i] = -1;
     group_bar();
     return sPart;
@@ -283,15 +283,18 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   for (int w = 1; w < NW; ++w) mstar = fmaxf(mstar, gred_f[w]);
   // W_c = 2^(m_c - m*) l_c: the power in fp32 (ex2.approx, 2 ulp) -- the fp32 scores already carry
   // errors of that order -- and everything downstream (products, sums, CDF) in fp64
-  double wv[kCPT];
+  // W_c in fp32 (<= 1.5e-7 relative: the ex2 and one rounding), sums and the CDF in fp64
+  float wv[kCPT];
   double part = 0.0;
   int lastpos = -1;
 #pragma unroll
   for (int i = 0; i < kCPT; ++i) {
-    wv[i] = lreg[i] > 0.f ? (double)ex2(mreg[i] - mstar) * (double)lreg[i] : 0.0;
-    part += wv[i];
-    if (wv[i] > 0.0) lastpos = c0 + i;
+    wv[i] = lreg[i] > 0.f ? ex2(mreg[i] - mstar) * lreg[i] : 0.f;
+    if (wv[i] > 0.f) lastpos = c0 + i;
   }
+#pragma unroll
+  for (int i = 0; i < kCPT; ++i) part += (double)wv[i];
+  if (sy.trace && tid == 0 && tslot >= 0) sy.trace[(size_t)blockIdx.x * kTraceStride + 120 + (tslot - 24) / 10 * 2] = gtimer();
   {
     const double incl = warp_incl_scan_d(part, lane);
     int lp = lastpos;
@@ -300,6 +303,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
     if (lane == 31) gred_d[wg] = incl;
     if (lane == 0) gred_i[wg] = lp;
     group_bar();
+    if (sy.trace && tid == 0 && tslot >= 0) sy.trace[(size_t)blockIdx.x * kTraceStride + 121 + (tslot - 24) / 10 * 2] = gtimer();
     double off = 0.0, Z = 0.0;
     int lpos = -1;
 #pragma unroll
@@ -314,9 +318,9 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
 #pragma unroll
     for (int i = 0; i < kCPT; ++i) {
       if (i < nmine) {
-        run += wv[i];
+        run += (double)wv[i];
         sF[c0 + i] = c0 + i >= lpos ? 1.0 : run * invZ;
-        sR[c0 + i] = wv[i];
+        sR[c0 + i] = (double)wv[i];
       }
     }
     if (tid == 0) gZ = Z;
@@ -400,24 +404,23 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
       const int kb = 4 * l, n = nn[u];
       // k1 = #{k < n : q[k] <= tq} = min{k : q[k] > tq}; k2 = #{k < n : q[k] < qmax} = the first key
       // reaching the chunk's full mass (used when rounding puts tq at/after it)
-      // the tag byte makes every word > tq unless compared on the low 24 bits; words of keys >= n
-      // hold the full mass (kQMax) and are excluded by the bound
-      const int k1 = __popc(__ballot_sync(0xffffffffu, on && kb < n && (v.x & kQMax) <= tq) & hmask) +
-                     __popc(__ballot_sync(0xffffffffu, on && kb + 1 < n && (v.y & kQMax) <= tq) & hmask) +
-                     __popc(__ballot_sync(0xffffffffu, on && kb + 2 < n && (v.z & kQMax) <= tq) & hmask) +
-                     __popc(__ballot_sync(0xffffffffu, on && kb + 3 < n && (v.w & kQMax) <= tq) & hmask);
-      int k = k1;
-      if (__any_sync(0xffffffffu, on && k1 >= n)) {  // rare: rounding put tq at/after the chunk's full mass
-        const int k2 = __popc(__ballot_sync(0xffffffffu, on && kb < n && (v.x & kQMax) < kQMax) & hmask) +
-                       __popc(__ballot_sync(0xffffffffu, on && kb + 1 < n && (v.y & kQMax) < kQMax) & hmask) +
-                       __popc(__ballot_sync(0xffffffffu, on && kb + 2 < n && (v.z & kQMax) < kQMax) & hmask) +
-                       __popc(__ballot_sync(0xffffffffu, on && kb + 3 < n && (v.w & kQMax) < kQMax) & hmask);
-        if (k1 >= n) k = k2;  // the first key reaching the full mass = the last positive-mass key
-      }
+      // q is non-decreasing over the chunk's keys (words of keys >= n hold the full mass kQMax and
+      // are masked to it), so k = #{k : q[k] <= tq} is found with ONE ballot over every lane's last
+      // word (lane j's 4 keys are 4j..4j+3) plus the crossing lane's own count of its 4 words.
+      // With tq >= the full mass (rounding) the count runs to n; then the last positive-mass key,
+      // the first key holding the full mass, is taken instead.
+      const uint32_t qx = kb < n ? (v.x & kQMax) : kQMax, qy = kb + 1 < n ? (v.y & kQMax) : kQMax;
+      const uint32_t qz = kb + 2 < n ? (v.z & kQMax) : kQMax, qw = kb + 3 < n ? (v.w & kQMax) : kQMax;
+      const uint32_t tqe = tq < kQMax ? tq : kQMax - 1u;  // q <= tqe <=> q <= tq, except at the full mass
+      const int full_lanes = __popc(__ballot_sync(0xffffffffu, qw <= tqe) & hmask);  // lanes entirely <= tq
+      const int own = (qx <= tqe) + (qy <= tqe) + (qz <= tqe) + (qw <= tqe);
+      const int cross = __shfl_sync(0xffffffffu, own, (tid & 16) + min(full_lanes, 15));
+      int k = full_lanes < 16 ? 4 * full_lanes + cross : 64;  // first k with q[k] > tqe
+      k = min(k, n - 1);
       jj[u] = -1;
       if (on) {
         jj[u] = cc[u] * 64 + min(k, n - 1);
-        if (l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u];
+        if (l == 0 && p.idx_out && !dry) p.idx_out[bh * S + m_lo + m] = jj[u];
       }
     }
     if (tid == 0 && tslot >= 0 && mw == 0) STEP_TRACE(tslot + 9);
@@ -695,11 +698,11 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
     const float invS = 1.0f / (float)sp.S;
     const int gtid = threadIdx.x - 32 * (NW + 1);
     __shared__ uint32_t sTicket;
-    for (int it = blockIdx.x, ord = 0; it < items; it += grid, ++ord) {
+    for (int it = blockIdx.x, ord = 0; it < items;) {
       const int rank = it % CS, bh = it / CS;
       const int b = bh / sp.H, h = bh - b * sp.H;
       const int tslot = (sy.trace && ord < 3) ? 24 + 10 * ord : -1;
-      const float* sPart = step_sample_item<T, D, G>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8);
+      const float* sPart = step_sample_item<T, D, G>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
       if (CS == 1) {
         for (int d = gtid; d < D; d += NSW * 32) store_out<T, D>(sp, (size_t)bh, d, sPart[d] * invS);
       } else {
@@ -712,18 +715,22 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
           if (gtid == 0) sy.head_ticket[bh] = 0u;
           const unsigned long long t0 = gtimer();
           for (int d = gtid; d < D; d += NSW * 32) {
+            unsigned long long v[kStepMaxSplits];
+#pragma unroll
+            for (int r = 0; r < kStepMaxSplits; ++r)  // all loads in flight at once
+              if (r < CS) v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
             float s = 0.f;
-            for (int r = 0; r < CS; ++r) {
-              const unsigned long long* src = sy.part + ((size_t)bh * CS + r) * D + d;
-              unsigned long long v = ld_strong_u64(src);
-              while ((uint32_t)(v >> 32) != tag32) {
+#pragma unroll
+            for (int r = 0; r < kStepMaxSplits; ++r) {
+              if (r >= CS) break;
+              while ((uint32_t)(v[r] >> 32) != tag32) {  // rare: a partial not yet visible
                 if (poll_expired(t0)) {
                   atomicOr(sp.flags, SANTA_FLAG_SYNC_TIMEOUT);
                   break;
                 }
-                v = ld_strong_u64(src);
+                v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
               }
-              s += __uint_as_float((uint32_t)v);
+              s += __uint_as_float((uint32_t)v[r]);  // fixed split order
             }
             store_out<T, D>(sp, (size_t)bh, d, s * invS);
           }
@@ -732,6 +739,8 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
       if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 6);
       group_bar();  // sPart / sTicket are rewritten by the next item
       if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 7);
+      it += grid;
+      ++ord;
     }
   }
   // ---------------- exit ticket: the last CTA out advances the epoch ----------------

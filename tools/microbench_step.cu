@@ -243,8 +243,40 @@ int main(int argc, char** argv) {
         if (k) dur[k].push_back((double)(x[order[k]] - x[order[k - 1]]) * 1e-3);
       }
     }
+  {
+    std::vector<double> a1, a2, a3;
+    for (int c = 0; c < nsm; ++c)
+      for (int i = 0; i < 3; ++i) {
+        const unsigned long long* x = &tr[(size_t)c * kTraceStride + 24 + 10 * i];
+        const unsigned long long* y = &tr[(size_t)c * kTraceStride + 120 + 2 * i];
+        if (!x[0] || !x[7] || !y[0]) continue;
+        a1.push_back((double)(y[0] - x[2]) * 1e-3);
+        a2.push_back((double)(y[1] - y[0]) * 1e-3);
+        a3.push_back((double)(x[3] - y[1]) * 1e-3);
+      }
+    stat("CDF: weights (ex2, fp64 mul)", a1);
+    stat("CDF: warp scans + group bar", a2);
+    stat("CDF: offsets, 1/Z, F, bar", a3);
+  }
   printf("sampler items, absolute times:\n");
   for (int k = 0; k < 10; ++k) stat(pn[k], abs_[k]);
+  {  // the three items that finish last: their own timelines
+    std::vector<std::pair<unsigned long long, std::pair<int, int>>> ends;
+    for (int c = 0; c < nsm; ++c)
+      for (int i = 0; i < 3; ++i) {
+        const unsigned long long* x = &tr[(size_t)c * kTraceStride + 24 + 10 * i];
+        if (x[0] && x[7]) ends.push_back({x[7], {c, i}});
+      }
+    std::sort(ends.begin(), ends.end());
+    for (size_t e = ends.size() >= 3 ? ends.size() - 3 : 0; e < ends.size(); ++e) {
+      const int c = ends[e].second.first, i = ends[e].second.second;
+      const unsigned long long* x = &tr[(size_t)c * kTraceStride + 24 + 10 * i];
+      const unsigned long long* y = &tr[(size_t)c * kTraceStride + 120 + 2 * i];
+      printf("  last item (CTA %d):", c);
+      for (int k = 0; k < 10; ++k) printf(" %s=%.2f", pn[k], rel(x[order[k]]));
+      printf(" | cdf: weights=%.2f scans=%.2f\n", rel(y[0]), rel(y[1]));
+    }
+  }
   printf("sampler items, phase durations (from the previous point):\n");
   for (int k = 1; k < 10; ++k) stat(pn[k], dur[k]);
   return 0;
