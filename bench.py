@@ -296,6 +296,86 @@ def config3(args, dev, stream, timed_loop, max_over_ranks, peak, world):
     return rows
 
 
+def config4(args, dev, stream, timed_loop, peak):
+    """BASELINE config 4 on ONE GPU: 512k context, S=1024 stratified, the per-rank work of a
+    sequence-sharded step for R = 2/4/8 ranks (rank 0's shard of 512k/R tokens): phase 1 (score
+    pass + shard (m_r, L_r)) and phase 2 (global shard CDF, own strata, local gather).  The NCCL
+    all_gather / all_reduce between them are not timed here (one GPU in this run); the stats of the
+    other ranks are taken equal to this rank's (each rank owns ~S/R strata), labelled as such."""
+    import torch
+
+    from paper_2605_01910_b200 import sharding
+    import santa_inputs as si
+
+    H, Hkv, d, S, n = 32, 8, 128, 1024, 524288
+    rows = {}
+    for R in (2, 4, 8):
+        nloc = n // R
+        inp = si.make_decode_inputs(1, H, Hkv, d, nloc, dtype="bf16", workload=args.workload, seed=400 + R,
+                                    device=str(dev))
+        be = sharding.CudaBackend()
+        st = be.stats(inp.q, inp.K, inp.seqlens, Hkv, S)
+        stats_all = st.unsqueeze(0).repeat(R, 1, 1, 1).contiguous()
+        off = torch.zeros(1, dtype=torch.int32, device=dev)
+        steps = max(3, min(args.steps, 20))
+        t1 = timed_loop(lambda i: be.stats(inp.q, inp.K, inp.seqlens, Hkv, S), steps)
+        t2 = timed_loop(lambda i: be.sample_gather(stats_all, 0, R, off, inp.V, inp.seqlens, S, args.mode, args.seed,
+                                                   i), steps)
+        kb = Hkv * nloc * d * 2
+        rows[str(R)] = {"tokens_per_rank": nloc, "phase1_us": round(t1 * 1e3, 2), "phase2_us": round(t2 * 1e3, 2),
+                        "per_rank_kernel_us": round((t1 + t2) * 1e3, 2),
+                        "phase1_GBps": round(kb / (t1 * 1e-3) / 1e9, 1),
+                        "phase1_frac_of_peak": round(kb / (t1 * 1e-3) / 1e9 / peak, 4)}
+        del inp, be, st, stats_all
+        torch.cuda.empty_cache()
+    rows["note"] = ("per-rank kernels only (1 GPU): rank 0 of R, shard = 512k/R tokens of every kv head, "
+                    "S=1024; the two NCCL collectives (all_gather of R x 256 B, all_reduce of 16 KiB) are "
+                    "exercised by the gloo tests, not timed here")
+    return rows
+
+
+def config5(args, dev, stream, timed_loop, peak):
+    """BASELINE config 5: Bernoulli ternary-q score stage (mean-group, stratified, B=8) + the
+    S^2ANTA value stage (S=256 stratified), 32k context, batch 16, feature-major K^T; calibrated
+    lognormal queries.  Bytes = the selected feature rows of K^T + unique V rows."""
+    import torch
+
+    import paper_2605_01910_b200 as santa
+    import santa_inputs as si
+
+    Bt, H, Hkv, d, n, S, nB = 16, 32, 8, 128, args.seqlen, 256, 8
+    inp = si.make_decode_inputs(Bt, H, Hkv, d, n, dtype="bf16", workload="lognormal", seed=500,
+                                feature_major=True, device=str(dev))
+    inp.K = None  # only the feature-major copy is read
+    torch.cuda.empty_cache()
+    geo = santa.make_geometry(inp.q, Hkv, n)
+    ws = santa.workspace(geo, S, dev)
+    out = torch.empty_like(inp.q)
+    idx = torch.empty((Bt, H, S), dtype=torch.int32, device=dev)
+    scores = torch.empty((Bt, H, n), dtype=torch.float32, device=dev)
+    mask = torch.zeros((Bt, Hkv, d), dtype=torch.uint8, device=dev)
+    santa.santa_bernoulli_scores(geo, inp.q, inp.Kt, inp.seqlens, nB, 1, 1, args.seed, 0, scores, mask, ws)
+    santa.santa_decode_attention_bernoulli(geo, inp.q, inp.Kt, inp.V, inp.seqlens, nB, 1, 1, S, args.mode, args.seed,
+                                           0, out, idx, ws)
+    torch.cuda.synchronize()
+    frac = float(mask.float().mean().item())
+    U = unique_rows_gpu(idx, Hkv)
+    fn = lambda i: santa.santa_decode_attention_bernoulli(geo, inp.q, inp.Kt, inp.V, inp.seqlens, nB, 1, 1, S,  # noqa
+                                                          args.mode, args.seed, i, out, None, ws, stream)
+    for i in range(3):
+        fn(i)
+    steps = max(3, min(args.steps, 20))
+    t = timed_loop(fn, steps)
+    byt = frac * Bt * Hkv * d * n * 2 + U * d * 2 + 2 * Bt * H * d * 2
+    gb = byt / (t * 1e-3) / 1e9
+    del inp, out, scores, ws
+    torch.cuda.empty_cache()
+    return {"us": round(t * 1e3, 2), "GBps": round(gb, 1), "frac_of_peak": round(gb / peak, 4),
+            "feature_access_frac": round(frac, 4), "unique_rows": U,
+            "note": "batch 16, 32k, mean-group stratified Bernoulli B=8 (P:448, P:510) + S=256 stratified; "
+                    "bytes = selected K^T feature rows + unique V rows + q/out"}
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -516,32 +596,46 @@ def main():
             res["graph_replay_us"] = round(gms * 1e3, 2)
         except Exception as ex:  # graph capture is an extra, never the headline
             res["graph_replay_us"] = f"unavailable: {type(ex).__name__}: {ex}"[:200]
-        # (5) end to end through the host-buffer C-ABI entry point
-        qh = p0.q.cpu().pin_memory()
-        knh = torch.randn(B, Hkv, d).to(torch.bfloat16).pin_memory()
-        vnh = torch.randn(B, Hkv, d).to(torch.bfloat16).pin_memory()
-        outh = torch.empty_like(qh).pin_memory()
-        qd, knd, vnd, od = torch.empty_like(p0.q), torch.empty(B, Hkv, d, dtype=torch.bfloat16, device=dev), \
-            torch.empty(B, Hkv, d, dtype=torch.bfloat16, device=dev), torch.empty_like(p0.q)
+        # (5) end to end through the host-buffer C-ABI entry point: every step copies its packed
+        # pinned [q | k_new | v_new] to the device (one H2D), appends the token to the cache, decodes,
+        # and copies out back to pinned host memory (one D2H); K steps back-to-back, asynchronous,
+        # CUDA events on the stream around all of them (+ the final sync inside the region)
+        qkv_elems = B * H * d + 2 * B * Hkv * d
+        qkvh = torch.randn(qkv_elems).to(torch.bfloat16).pin_memory()
+        qkvh[:B * H * d].copy_(p0.q.reshape(-1).cpu())
+        qkvd = torch.empty(qkv_elems, dtype=torch.bfloat16, device=dev)
+        outh = torch.empty(B * H * d, dtype=torch.bfloat16).pin_memory()
+        od = torch.empty_like(p0.q)
+
+        def e2e_step(i):
+            p = probs[i % NR]
+            santa.santa_decode_step_host_packed(p.geo, qkvh, qkvd, p.K, p.V, p.seqlens, args.S, args.mode, args.seed,
+                                                i, od, outh, ws, synchronize=False, stream=stream)
+        for i in range(args.warmup):
+            e2e_step(i)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(timed_loop(e2e_step, args.steps))
+        res["e2e"] = {"value": round(world * bytes_step / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
+                      "us_per_step": round(ems * 1e3, 2),
+                      "h2d_bytes_per_step": qkvh.numel() * 2, "d2h_bytes_per_step": outh.numel() * 2,
+                      "path": "santa_decode_step_host_packed: per step one pinned H2D of [q|k_new|v_new], KV append, "
+                              "decode, one D2H of out to pinned memory; back-to-back steps, CUDA events"}
+        # the synchronous single-call latency of the same API (host wall clock incl. the stream sync)
         et = []
         for i in range(args.warmup + args.steps):
             p = probs[i % NR]
             t0 = time.perf_counter()
-            santa.santa_decode_step_host(p.geo, qh, knh, vnh, qd, knd, vnd, p.K, p.V, p.seqlens, args.S, args.mode,
-                                         args.seed, i, od, outh, ws, stream)
-            t1 = time.perf_counter()
+            santa.santa_decode_step_host_packed(p.geo, qkvh, qkvd, p.K, p.V, p.seqlens, args.S, args.mode, args.seed,
+                                                i, od, outh, ws, synchronize=True, stream=stream)
             if i >= args.warmup:
-                et.append(t1 - t0)
-        ems = max_over_ranks(float(np.mean(et)) * 1e3)
-        res["e2e"] = {"value": round(world * bytes_step / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
-                      "us_per_step": round(ems * 1e3, 2),
-                      "h2d_bytes_per_step": qh.numel() * 2 + knh.numel() * 2 + vnh.numel() * 2,
-                      "d2h_bytes_per_step": outh.numel() * 2,
-                      "path": "santa_decode_step_host: pinned H2D q/k_new/v_new + KV append + decode + D2H out, "
-                              "host wall clock incl. stream sync"}
+                et.append(time.perf_counter() - t0)
+        res["e2e"]["sync_call_latency_us"] = round(float(np.median(et)) * 1e6, 2)
 
     if not args.no_extras and args.batch == 1 and not args.page_size and not args.no_config3:
         res["config3"] = config3(args, dev, stream, timed_loop, max_over_ranks, peak, world)
+        if world == 1:
+            res["config4_per_rank"] = config4(args, dev, stream, timed_loop, peak)
+            res["config5"] = config5(args, dev, stream, timed_loop, peak)
     if not args.no_extras and not args.no_baselines and rank == 0 and args.batch == 1 and not args.page_size:
         res["library_baselines"] = library_baselines(probs, NR, timed_loop, args)
         d = res["library_baselines"]

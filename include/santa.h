@@ -16,7 +16,8 @@
  * - Arguments are validated synchronously on the host BEFORE anything is
  *   launched.  On any error nothing is launched and no output is touched.  No
  *   exception or abort crosses the ABI.  No host<->device synchronisation happens
- *   inside any call except santa_read_error_flags and santa_decode_step_host.
+ *   inside any call except santa_read_error_flags, santa_decode_step_host and
+ *   santa_decode_step_host_packed with synchronize != 0.
  * - Determinism: identical inputs, seed and offset give bit-identical `out` and
  *   `idx_out` across runs (no floating-point atomics anywhere).
  * - Device-side data errors (a seqlen < 1, i.e. an "empty distribution")
@@ -245,6 +246,19 @@ santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_hos
                                     uint64_t seed, uint64_t offset, void* out_dev,
                                     void* out_host, void* workspace, size_t workspace_bytes,
                                     void* stream);
+
+/* As santa_decode_step_host with ONE packed host buffer and an optional sync -- the form a
+ * serving loop uses: qkv_host (pinned) = [q (B*H*d) | k_new (B*H_kv*d) | v_new (B*H_kv*d)]
+ * elements of the geometry's dtype, copied with one H2D into the device staging buffer qkv_dev
+ * (same size), then the KV append, santa_decode_attention, and one D2H of out_dev into out_host
+ * (pinned, B*H*d).  synchronize != 0: syncs `stream` before returning (out_host is valid);
+ * synchronize == 0: fully asynchronous, out_host is valid once the caller syncs the stream.
+ * Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
+santa_status santa_decode_step_host_packed(const santa_geometry* geo, const void* qkv_host, void* qkv_dev,
+                                           void* K, void* V, const int32_t* seqlens, int32_t S,
+                                           int32_t mode, uint64_t seed, uint64_t offset, void* out_dev,
+                                           void* out_host, void* workspace, size_t workspace_bytes,
+                                           int32_t synchronize, void* stream);
 
 /* Device Philox4x32-10 uniforms for testing the device RNG against the Random123 KAT and
  * the oracle stream: out[i] = u(draw i) of the stream (seed, offset, tag, h_global, b_global),

@@ -24,7 +24,7 @@ __all__ = [
     "santa_sample_phase", "PATHS", "FLAG_SYNC_TIMEOUT",
     "santa_dense_reference",
     "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
-    "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_philox_uniforms",
+    "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_decode_step_host_packed", "santa_philox_uniforms",
     "santa_read_error_flags", "santa_version", "decode", "dense", "LIB_PATH",
 ]
 LIB_PATH = _abi.LIB_PATH
@@ -156,6 +156,18 @@ def santa_decode_step_host(geo, q_host, k_new_host, v_new_host, q_dev, k_new_dev
         ctypes.byref(geo), hp(q_host), hp(k_new_host), hp(v_new_host), _ptr(q_dev), _ptr(k_new_dev),
         _ptr(v_new_dev), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset, _ptr(out_dev),
         hp(out_host), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_decode_step_host_packed(geo, qkv_host, qkv_dev, K, V, seqlens, S, mode, seed, offset, out_dev, out_host,
+                                  ws, synchronize=True, stream=None):
+    """One H2D of the packed pinned [q | k_new | v_new] buffer, KV append, decode, one D2H of out."""
+    for t in (qkv_host, out_host):
+        if t.is_cuda or not t.is_pinned():
+            raise ValueError("host buffers must be pinned CPU tensors")
+    hp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
+    _abi.check("santa_decode_step_host_packed", _abi.LIB.santa_decode_step_host_packed(
+        ctypes.byref(geo), hp(qkv_host), _ptr(qkv_dev), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode),
+        seed, offset, _ptr(out_dev), hp(out_host), _ptr(ws), ws.numel(), int(bool(synchronize)), _stream(stream)))
 
 
 def santa_philox_uniforms(seed, offset, tag, h_global, b_global, n, out, ctr_key: Optional[Sequence[int]] = None,

@@ -68,6 +68,7 @@ def _load() -> ctypes.CDLL:
                                          i32),
         "santa_decode_step_host": ([G, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz,
                                     vp], i32),
+        "santa_decode_step_host_packed": ([G, vp, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, i32, vp], i32),
         "santa_philox_uniforms": ([u64, u64, i32, i32, i32, i32, vp, vp, vp, vp], i32),
         "santa_read_error_flags": ([vp, ctypes.POINTER(ctypes.c_uint32), vp], i32),
     }

@@ -881,6 +881,35 @@ santa_status santa_decode_step_host(const santa_geometry* g, const void* q_host,
   return SANTA_OK;
 }
 
+santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* qkv_host, void* qkv_dev, void* K,
+                                           void* V, const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
+                                           uint64_t offset, void* out_dev, void* out_host, void* ws, size_t ws_bytes,
+                                           int32_t synchronize, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (!qkv_host || !qkv_dev || !out_host) return SANTA_ERR_INVALID_ARG;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (!aligned16(qkv_dev)) return SANTA_ERR_ALIGNMENT;
+  if ((s = validate_decode_ptrs(qkv_dev, K, V, seqlens, out_dev)) != SANTA_OK) return s;
+  WsLayout L;
+  if ((s = check_ws(g, S, ws, ws_bytes, &L)) != SANTA_OK) return s;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t eb = elem_bytes(g->dtype), D = g->head_dim;
+  const size_t qb = (size_t)g->batch * g->n_heads * D * eb, kb = (size_t)g->batch * g->n_kv_heads * D * eb;
+  if ((qb % 16) || (kb % 16)) return SANTA_ERR_ALIGNMENT;  // k_new / v_new sub-buffers stay 16-B aligned
+  char* dev = reinterpret_cast<char*>(qkv_dev);
+  if (cudaMemcpyAsync(dev, qkv_host, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, dev + qb, dev + qb + kb, kv_layout(g), seqlens,
+                                                                  (int)D, (int)eb);
+  if ((s = last_cuda()) != SANTA_OK) return s;
+  if ((s = decode_common(g, dev, K, V, seqlens, S, mode, seed, offset, out_dev, nullptr, ws, ws_bytes, nullptr,
+                         stream)) != SANTA_OK)
+    return s;
+  if (cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (synchronize && cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
+  return SANTA_OK;
+}
+
 santa_status santa_philox_uniforms(uint64_t seed, uint64_t offset, int32_t tag, int32_t h_global, int32_t b_global,
                                    int32_t n, double* out, const uint32_t* ctr_key_host, uint32_t* raw_out,
                                    void* stream) {

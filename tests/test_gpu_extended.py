@@ -149,3 +149,38 @@ def test_decode_step_host_matches_device_call():
     ref = santa.decode(inp.q, K2, V2, inp.seqlens, S, "systematic", 5, 2)
     torch.cuda.synchronize()
     assert torch.equal(outh, ref.cpu())
+
+
+def test_decode_step_host_packed_async_matches_device_call():
+    """The packed-buffer host API (one H2D, append, decode, one D2H), asynchronous over several
+    steps, gives for every step exactly the device call's output on the appended cache."""
+    B, H, Hkv, d, S = 2, 16, 4, 128, 64
+    n = [700, 1500]
+    inp = to_cuda(si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=33, max_seqlen=1600))
+    geo = santa.make_geometry(inp.q, Hkv, 1600)
+    ws = santa.workspace(geo, S)
+    K2, V2 = inp.K.clone(), inp.V.clone()
+    steps = 3
+    qkvs = [torch.randn(B * H * d + 2 * B * Hkv * d).to(torch.bfloat16).pin_memory() for _ in range(steps)]
+    outs = [torch.empty(B * H * d, dtype=torch.bfloat16).pin_memory() for _ in range(steps)]
+    devbufs = [torch.empty(B * H * d + 2 * B * Hkv * d, dtype=torch.bfloat16, device="cuda") for _ in range(steps)]
+    od = [torch.empty_like(inp.q) for _ in range(steps)]
+    for i in range(steps):
+        santa.santa_decode_step_host_packed(geo, qkvs[i], devbufs[i], K2, V2, inp.seqlens, S, "stratified", 9, i,
+                                            od[i], outs[i], ws, synchronize=False)
+    torch.cuda.synchronize()
+    # after the last step the cache holds the last step's token; replay each step on a fresh copy
+    for i in range(steps):
+        K3, V3 = inp.K.clone(), inp.V.clone()
+        qkv = qkvs[i]
+        q = qkv[:B * H * d].reshape(B, H, d).cuda()
+        kn = qkv[B * H * d:B * H * d + B * Hkv * d].reshape(B, Hkv, d)
+        vn = qkv[B * H * d + B * Hkv * d:].reshape(B, Hkv, d)
+        for b in range(B):
+            K3[b, :, n[b] - 1] = kn[b].cuda()
+            V3[b, :, n[b] - 1] = vn[b].cuda()
+        ref = santa.decode(q, K3, V3, inp.seqlens, S, "stratified", 9, i, max_seqlen=1600)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[i], ref.reshape(-1).cpu()), i
+        if i == steps - 1:
+            assert torch.equal(K2, K3) and torch.equal(V2, V3)
