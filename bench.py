@@ -631,8 +631,9 @@ def main():
                 et.append(time.perf_counter() - t0)
         res["e2e"]["sync_call_latency_us"] = round(float(np.median(et)) * 1e6, 2)
 
-    if not args.no_extras and args.batch == 1 and not args.page_size and not args.no_config3:
-        res["config3"] = config3(args, dev, stream, timed_loop, max_over_ranks, peak, world)
+    if not args.no_extras and args.batch == 1 and not args.page_size:
+        if not args.no_config3:
+            res["config3"] = config3(args, dev, stream, timed_loop, max_over_ranks, peak, world)
         if world == 1:
             res["config4_per_rank"] = config4(args, dev, stream, timed_loop, peak)
             res["config5"] = config5(args, dev, stream, timed_loop, peak)

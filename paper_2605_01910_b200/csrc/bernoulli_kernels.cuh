@@ -44,6 +44,7 @@ struct BernParams {
   float* stash;
   float2* cstats;
   int Cmax, stash_stride;
+  int sub64;                // 1: stats/stash per 64-key sub-chunk (Cmax/stash_stride of the L = 64 layout)
   uint32_t* tickets;
   uint32_t* flags;
 };
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
 }
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams p) {
+__global__ void __launch_bounds__(kScoreThreads, 4) bern_chunk_kernel(BernParams p) {
   __shared__ __align__(16) float sS[G * kDenseChunk];
   __shared__ __align__(16) float sAcc[4][G][kDenseChunk];
   __shared__ float sW[G][D];
@@ -144,9 +145,13 @@ __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams
   const int n_valid = min(kDenseChunk, seqlen - chunk_start);
   const size_t unit = (size_t)b * p.Hkv + kvh;
   const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
-  float2* cst = p.cstats + bh0 * p.Cmax + c;
+  // stats/stash granularity: 64-key sub-chunks (sub64: the standard decode layout, 4 per CTA) or
+  // the whole 256-key chunk
+  const int cpc = p.sub64 ? kDenseChunk / 64 : 1;
+  float2* cst = p.cstats + bh0 * p.Cmax + (size_t)c * cpc;
   if (n_valid <= 0) {
-    if (threadIdx.x < G) cst[(size_t)threadIdx.x * p.Cmax] = make_float2(-INFINITY, 0.f);
+    if (threadIdx.x < G * cpc && (size_t)c * cpc + threadIdx.x % cpc < (size_t)p.Cmax)
+      cst[(size_t)(threadIdx.x / cpc) * p.Cmax + threadIdx.x % cpc] = make_float2(-INFINITY, 0.f);
     if (p.scores && chunk_start < p.score_stride)
       for (int t = threadIdx.x; t < G * kDenseChunk; t += kScoreThreads) {
         const int k = chunk_start + t % kDenseChunk;
@@ -171,30 +176,45 @@ __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
   const bool live = kl < n_valid;
-  for (int s = warp; s < nsel; s += 4) {
-    const int i = sSel[s];
-    float v[8];
-    if (live) {
-      const T* src = Kt + (int64_t)i * P;
+  // UF selected feature rows per warp in flight (16-B loads issued before any is consumed): one load
+  // per lane per feature leaves ~6 KiB in flight per SM, far below what HBM needs (measured 0.37 of peak)
+  constexpr int UF = sizeof(T) == 2 ? 8 : 4;
+  for (int s0 = warp; s0 < nsel; s0 += 4 * UF) {
+    uint4 r[UF][sizeof(T) == 2 ? 1 : 2];
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int s = s0 + 4 * u;
+      if (live && s < nsel) {
+        const T* src = Kt + (int64_t)sSel[s] * P;
+        r[u][0] = ldg_stream(src);
+        if constexpr (sizeof(T) == 4) r[u][1] = ldg_stream(src + 4);
+      } else {
+        r[u][0] = make_uint4(0u, 0u, 0u, 0u);
+        if constexpr (sizeof(T) == 4) r[u][1] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UF; ++u) {
+      const int s = s0 + 4 * u;
+      if (s >= nsel) break;
+      const int i = sSel[s];
+      float v[8];
       if constexpr (sizeof(T) == 2) {
-        const uint4 r = ldg_stream(src);
-        const uint32_t wv[4] = {r.x, r.y, r.z, r.w};
+        const uint32_t wv[4] = {r[u][0].x, r[u][0].y, r[u][0].z, r[u][0].w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) { v[2 * e] = Elem<T>::lo(wv[e]); v[2 * e + 1] = Elem<T>::hi(wv[e]); }
       } else {
-        const uint4 r0 = ldg_stream(src), r1 = ldg_stream(src + 4);
-        v[0] = __uint_as_float(r0.x); v[1] = __uint_as_float(r0.y); v[2] = __uint_as_float(r0.z); v[3] = __uint_as_float(r0.w);
-        v[4] = __uint_as_float(r1.x); v[5] = __uint_as_float(r1.y); v[6] = __uint_as_float(r1.z); v[7] = __uint_as_float(r1.w);
+        v[0] = __uint_as_float(r[u][0].x); v[1] = __uint_as_float(r[u][0].y);
+        v[2] = __uint_as_float(r[u][0].z); v[3] = __uint_as_float(r[u][0].w);
+        v[4] = __uint_as_float(r[u][1].x); v[5] = __uint_as_float(r[u][1].y);
+        v[6] = __uint_as_float(r[u][1].z); v[7] = __uint_as_float(r[u][1].w);
       }
-    } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = 0.f;
-    }
+      for (int g = 0; g < G; ++g) {
+        const float wg = sW[g][i];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float wg = sW[g][i];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(wg, v[e], acc[g][e]);
+        for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(wg, v[e], acc[g][e]);
+      }
     }
   }
 #pragma unroll
@@ -207,14 +227,24 @@ __global__ void __launch_bounds__(kScoreThreads, 3) bern_chunk_kernel(BernParams
     const int g = t / kDenseChunk, k = t % kDenseChunk;
     const float ph = ((sAcc[0][g][k] + sAcc[1][g][k]) + sAcc[2][g][k]) + sAcc[3][g][k];
     const bool valid = k < n_valid;
-    sS[g * kDenseChunk + k] = valid ? ph * sl2 : -INFINITY;
+    sS[p.sub64 ? ((k >> 6) * G + g) * 64 + (k & 63) : g * kDenseChunk + k] = valid ? ph * sl2 : -INFINITY;
     if (p.scores && chunk_start + k < p.score_stride)
       p.scores[(bh0 + g) * p.score_stride + chunk_start + k] = valid ? ph * p.scale : 0.f;
   }
   __syncthreads();
-  if (p.stash)
-    chunk_epilogue<G>(sS, kDenseChunk, n_valid, warp, 4, p.stash + bh0 * p.stash_stride + chunk_start,
-                      p.stash_stride, cst, p.Cmax);
+  if (p.stash) {
+    if (p.sub64) {  // warp w: sub-chunk w with the L = 64 register epilogue (all G heads at once)
+      const int sub_start = chunk_start + 64 * warp, n_sub = min(64, seqlen - sub_start);
+      if (n_sub > 0)
+        warp_chunk_epilogue<G>(sS + warp * G * 64, 64, n_sub, p.stash + bh0 * p.stash_stride + sub_start,
+                               p.stash_stride, cst + warp, p.Cmax);
+      else if (lane < G && (size_t)c * cpc + warp < (size_t)p.Cmax)
+        cst[(size_t)lane * p.Cmax + warp] = make_float2(-INFINITY, 0.f);
+    } else {
+      chunk_epilogue<G>(sS, kDenseChunk, n_valid, warp, 4, p.stash + bh0 * p.stash_stride + chunk_start,
+                        p.stash_stride, cst, p.Cmax);
+    }
+  }
 }
 
 }  // namespace santa

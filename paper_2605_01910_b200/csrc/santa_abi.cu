@@ -33,7 +33,7 @@ struct WsLayout {
   size_t step_rec = 0, step_stash = 0, step_part = 0;  // step kernel's tagged regions
 };
 
-constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 1024 chunks of <= 1024 keys
+constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 8192 chunks of <= 128 keys
 
 int elem_bytes(int dtype) { return dtype == SANTA_F32 ? 4 : 2; }
 
@@ -61,10 +61,11 @@ WsLayout layout(const santa_geometry* g, int S) {
   WsLayout L;
   const int G = g->n_heads / g->n_kv_heads;
   const size_t B = g->batch, H = g->n_heads, Hkv = g->n_kv_heads, D = g->head_dim;
-  // SANTA chunk length: the smallest multiple of 64 keeping <= 1024 chunks per sequence
-  // (fine-grained work for the persistent score pass, bounded CDF tables for the sampler)
+  // SANTA chunk length: 64 keys (the fast register epilogue and ballot search) up to 8192 chunks
+  // per sequence (512k tokens: the sampler's fp64 chunk-CDF tables take 16 B per chunk of shared
+  // memory); longer contexts double L until <= 8192 chunks
   L.L = 64;
-  while ((g->max_seqlen + L.L - 1) / L.L > 1024) L.L *= 2;
+  while ((g->max_seqlen + L.L - 1) / L.L > 8192) L.L *= 2;
   L.Cmax = (g->max_seqlen + L.L - 1) / L.L;
   L.Cmax256 = (g->max_seqlen + 255) / 256;  // dense reference / Bernoulli chunking
   size_t off = 0;
@@ -604,8 +605,11 @@ struct RunBern {
     p.score_stride = a.g->max_seqlen;
     p.stash = for_decode ? at<float>(a.ws, a.L.stash) : nullptr;
     p.cstats = at<float2>(a.ws, a.L.cstats);
-    p.Cmax = a.L.Cmax256;
-    p.stash_stride = a.L.Cmax256 * kDenseChunk;
+    // decode: 64-key stats/stash in the standard layout when L = 64 (the sampler's fast ballot
+    // search), else per 256-key chunk
+    p.sub64 = (for_decode && a.L.L == 64) ? 1 : 0;
+    p.Cmax = p.sub64 ? a.L.Cmax : a.L.Cmax256;
+    p.stash_stride = p.sub64 ? a.L.Cmax * 64 : a.L.Cmax256 * kDenseChunk;
     p.tickets = at<uint32_t>(a.ws, a.L.tickets);
     p.flags = at<uint32_t>(a.ws, a.L.flags);
     if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
@@ -800,8 +804,10 @@ santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const voi
   if ((s = dispatch<RunBern>(g->dtype, g->head_dim, G, a, Kt, (int)nB, (int)stratified, (int)mean_group,
                              (float*)nullptr, (uint8_t*)nullptr, true)) != SANTA_OK)
     return s;
-  a.Lc = kDenseChunk;
-  a.Cc = a.L.Cmax256;
+  if (a.L.L != 64) {  // stats per 256-key chunk (contexts > 512k)
+    a.Lc = kDenseChunk;
+    a.Cc = a.L.Cmax256;
+  }
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   return last_cuda();
 }
