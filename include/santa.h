@@ -80,7 +80,8 @@ typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q,
 typedef enum {
   SANTA_PATH_AUTO = 0,        /* the step kernel when eligible, else the two-kernel path          */
   SANTA_PATH_STEP_KERNEL = 1, /* force the single launch (SANTA_ERR_UNSUPPORTED if not eligible) */
-  SANTA_PATH_TWO_KERNEL = 2   /* score pass + PDL-chained sampler kernel                          */
+  SANTA_PATH_TWO_KERNEL = 2,  /* score pass + PDL-chained sampler kernel                          */
+  SANTA_PATH_STEP_TC = 3      /* the step kernel with its score stage on tcgen05 tensor cores    */
 } santa_path;
 
 typedef struct {

@@ -18,7 +18,7 @@ MODES = {"iid": 0, "stratified": 1, "systematic": 2}
 DTYPES = {"bf16": 0, "f32": 1, "f16": 2}
 FLAG_EMPTY_SEQ = 0x1
 FLAG_SYNC_TIMEOUT = 0x100
-PATHS = {"auto": 0, "step": 1, "two_kernel": 2}
+PATHS = {"auto": 0, "step": 1, "two_kernel": 2, "step_tc": 3}
 
 
 class SantaError(RuntimeError):

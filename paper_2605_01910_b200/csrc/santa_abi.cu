@@ -14,6 +14,7 @@
 #include "sample_kernels.cuh"
 #include "score_kernels.cuh"
 #include "step_kernel.cuh"
+#include "step_tc_kernel.cuh"
 
 using namespace santa;
 
@@ -182,6 +183,7 @@ struct DecodeArgs {
   int rank, world;
   const int32_t* token_offset;
   int Lc = 0, Cc = 0;         // chunking the sampler reads (0 => the SANTA layout L / Cmax)
+  bool tensor_core = false;   // step kernel: score stage on tcgen05 (step_tc_kernel.cuh)
 };
 
 int num_sms() {
@@ -219,6 +221,19 @@ bool make_kmap(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype, i
   cuuint32_t es[2] = {1, 1};
   return fn(m, dtype == SANTA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
             const_cast<void*>(K), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// q viewed as [B*H rows][D]; boxes of G rows x 64 elements, 128B swizzle (the tcgen05 B operand).
+bool make_qmap(CUtensorMap* m, const void* q, uint64_t rows, int D, int dtype, int G) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)D * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)G};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, dtype == SANTA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void*>(q), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -374,8 +389,63 @@ struct RunSample {
 // The whole step in one pipelined cooperative launch (step_kernel.cuh).  Returns
 // SANTA_ERR_UNSUPPORTED (nothing launched) when the configuration does not qualify, in which
 // case the caller runs the two-kernel path.
+StepSync make_step_sync(const DecodeArgs& a) {
+  StepSync sy;
+  uint32_t* base = at<uint32_t>(a.ws, a.L.sync);
+  sy.epoch = base;
+  sy.exit_ticket = base + 1;
+  sy.head_ticket = base + 2;
+  sy.rec = at<ulonglong2>(a.ws, a.L.step_rec);
+  sy.stash = at<uint32_t>(a.ws, a.L.step_stash);
+  sy.part = at<unsigned long long>(a.ws, a.L.step_part);
+  sy.trace = nullptr;
+  return sy;
+}
+
 template <typename T, int D, int G>
 struct RunStep {
+  // the tensor-core variant (santa_step_tc_kernel): 128-key tiles, pages of a multiple of 128
+  static santa_status run_tc(const DecodeArgs& a, const ScoreParams& sp, const SampleParams& pp, int CS, int grid) {
+    if constexpr (sizeof(T) != 2) {
+      return SANTA_ERR_UNSUPPORTED;
+    } else {
+      constexpr int NSW = kStepSamplers, NT = 32 * (kTcEGWarps + 2 + NSW);
+      if (a.g->page_table && a.g->page_size % kTcTileKeys != 0) return SANTA_ERR_UNSUPPORTED;
+      const size_t smem = step_tc_score_smem_bytes(D, G) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
+      if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;
+      auto kern = santa_step_tc_kernel<T, D, G, NSW>;
+      static size_t configured = 0;
+      if (smem > configured) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+          return SANTA_ERR_CUDA;
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
+          return SANTA_ERR_UNSUPPORTED;
+        configured = smem;
+      }
+      CUtensorMap tk, tq;
+      const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
+                                            : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
+      if (!make_kmap(&tk, a.K, rows, D, a.g->dtype, 64)) return SANTA_ERR_UNSUPPORTED;
+      if (!make_qmap(&tq, a.q, (uint64_t)a.g->batch * a.g->n_heads, D, a.g->dtype, G)) return SANTA_ERR_UNSUPPORTED;
+      StepSync sy = make_step_sync(a);
+      SampleParams pq = pp;
+      pq.cluster = CS;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = a.st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, kern, tk, tq, sp, pq, sy) != cudaSuccess) return SANTA_ERR_CUDA;
+      return SANTA_OK;
+    }
+  }
+
   static santa_status run(const DecodeArgs& a) {
     if constexpr (sizeof(T) != 2) {
       return SANTA_ERR_UNSUPPORTED;
@@ -392,6 +462,7 @@ struct RunStep {
       int CS = 1;
       while (CS * 2 <= kStepMaxSplits && CS * 64 < a.S && heads * CS * 2 <= 4 * grid) CS *= 2;
       pp.cluster = CS;
+      if (a.tensor_core) return run_tc(a, sp, pp, CS, grid);
       const size_t smem = step_score_smem_bytes(D, G, NW, SPW) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
       if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;  // 227 KiB per CTA minus static smem
       auto kern = santa_step_kernel<T, D, G, NW, SPW, NSW>;
@@ -412,15 +483,7 @@ struct RunStep {
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
       if (!make_kmap(&tm, a.K, rows, D, a.g->dtype, kStepStageKeys)) return SANTA_ERR_UNSUPPORTED;
-      StepSync sy;
-      uint32_t* base = at<uint32_t>(a.ws, a.L.sync);
-      sy.epoch = base;
-      sy.exit_ticket = base + 1;
-      sy.head_ticket = base + 2;
-      sy.rec = at<ulonglong2>(a.ws, a.L.step_rec);
-      sy.stash = at<uint32_t>(a.ws, a.L.step_stash);
-      sy.part = at<unsigned long long>(a.ws, a.L.step_part);
-      sy.trace = nullptr;
+      StepSync sy = make_step_sync(a);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
       cfg.blockDim = dim3(NT);
@@ -637,7 +700,7 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
                            void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
                            void* stream, int path = SANTA_PATH_AUTO) {
   santa_status s = validate_geometry(g);
-  if (path < SANTA_PATH_AUTO || path > SANTA_PATH_TWO_KERNEL) return SANTA_ERR_INVALID_ARG;
+  if (path < SANTA_PATH_AUTO || path > SANTA_PATH_STEP_TC) return SANTA_ERR_INVALID_ARG;
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
   if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
@@ -654,9 +717,10 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   // AUTO = the single-launch step kernel when eligible (measured >= the two-kernel path at every
   // batch size of config 3, tools/path_sweep.py)
   if (!a.events && path != SANTA_PATH_TWO_KERNEL) {
+    a.tensor_core = path == SANTA_PATH_STEP_TC;
     s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
     if (s == SANTA_OK) return last_cuda();
-    if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL) return s;
+    if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL || path == SANTA_PATH_STEP_TC) return s;
   }
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;

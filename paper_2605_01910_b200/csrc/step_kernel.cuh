@@ -470,6 +470,63 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   return sPart;
 }
 
+// The sampler-group work loop (items it = blockIdx.x + k * grid), shared by the step kernels.
+// Sampler warps are the LAST NSW warps of the CTA.
+template <typename T, int D, int G, int NSW>
+__device__ __forceinline__ void step_sampler_loop(const SampleParams& sp, const StepSync& sy, unsigned char* samp_smem,
+                                                  uint32_t tag32, uint32_t tag8) {
+  const int grid = gridDim.x;
+  const int gtid = threadIdx.x - (blockDim.x - NSW * 32);
+  __shared__ uint32_t sTicket;
+  const int CS = sp.cluster;
+  const int items = sp.B * sp.H * CS;
+  const float invS = 1.0f / (float)sp.S;
+  for (int it = blockIdx.x, ord = 0; it < items;) {
+    const int rank = it % CS, bh = it / CS;
+    const int b = bh / sp.H, h = bh - b * sp.H;
+    const int tslot = (sy.trace && ord < 3) ? 24 + 10 * ord : -1;
+    const float* sPart = step_sample_item<T, D, G>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
+    if (CS == 1) {
+      for (int d = gtid; d < D; d += NSW * 32) store_out<T, D>(sp, (size_t)bh, d, sPart[d] * invS);
+    } else {
+      const unsigned long long t = (unsigned long long)tag32 << 32;
+      for (int d = gtid; d < D; d += NSW * 32) st_u64(sy.part + (size_t)it * D + d, t | __float_as_uint(sPart[d]));
+      group_bar();
+      if (gtid == 0) sTicket = atomicAdd(sy.head_ticket + bh, 1u);
+      group_bar();
+      if (sTicket == (uint32_t)(CS - 1)) {  // last split of the head: fixed-order sum of all splits
+        if (gtid == 0) sy.head_ticket[bh] = 0u;
+        const unsigned long long t0 = gtimer();
+        for (int d = gtid; d < D; d += NSW * 32) {
+          unsigned long long v[kStepMaxSplits];
+#pragma unroll
+          for (int r = 0; r < kStepMaxSplits; ++r)  // all loads in flight at once
+            if (r < CS) v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
+          float s = 0.f;
+#pragma unroll
+          for (int r = 0; r < kStepMaxSplits; ++r) {
+            if (r >= CS) break;
+            while ((uint32_t)(v[r] >> 32) != tag32) {  // rare: a partial not yet visible
+              if (poll_expired(t0)) {
+                atomicOr(sp.flags, SANTA_FLAG_SYNC_TIMEOUT);
+                break;
+              }
+              v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
+            }
+            s += __uint_as_float((uint32_t)v[r]);  // fixed split order
+          }
+          store_out<T, D>(sp, (size_t)bh, d, s * invS);
+        }
+      }
+    }
+    if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 6);
+    group_bar();  // sPart / sTicket are rewritten by the next item
+    if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 7);
+    it += grid;
+    ++ord;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // kVar (tools/microbench_step.cu ablations only; 0 in the library): bit 0 = consumers skip the
 // MMA and epilogue (wait + release only), bit 1 = sampler warps exit immediately.
@@ -693,55 +750,7 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
     }
   } else if constexpr ((kVar & 2) == 0) {
     // ---------------- sampler group ----------------
-    const int CS = sp.cluster;
-    const int items = sp.B * sp.H * CS;
-    const float invS = 1.0f / (float)sp.S;
-    const int gtid = threadIdx.x - 32 * (NW + 1);
-    __shared__ uint32_t sTicket;
-    for (int it = blockIdx.x, ord = 0; it < items;) {
-      const int rank = it % CS, bh = it / CS;
-      const int b = bh / sp.H, h = bh - b * sp.H;
-      const int tslot = (sy.trace && ord < 3) ? 24 + 10 * ord : -1;
-      const float* sPart = step_sample_item<T, D, G>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
-      if (CS == 1) {
-        for (int d = gtid; d < D; d += NSW * 32) store_out<T, D>(sp, (size_t)bh, d, sPart[d] * invS);
-      } else {
-        const unsigned long long t = (unsigned long long)tag32 << 32;
-        for (int d = gtid; d < D; d += NSW * 32) st_u64(sy.part + (size_t)it * D + d, t | __float_as_uint(sPart[d]));
-        group_bar();
-        if (gtid == 0) sTicket = atomicAdd(sy.head_ticket + bh, 1u);
-        group_bar();
-        if (sTicket == (uint32_t)(CS - 1)) {  // last split of the head: fixed-order sum of all splits
-          if (gtid == 0) sy.head_ticket[bh] = 0u;
-          const unsigned long long t0 = gtimer();
-          for (int d = gtid; d < D; d += NSW * 32) {
-            unsigned long long v[kStepMaxSplits];
-#pragma unroll
-            for (int r = 0; r < kStepMaxSplits; ++r)  // all loads in flight at once
-              if (r < CS) v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
-            float s = 0.f;
-#pragma unroll
-            for (int r = 0; r < kStepMaxSplits; ++r) {
-              if (r >= CS) break;
-              while ((uint32_t)(v[r] >> 32) != tag32) {  // rare: a partial not yet visible
-                if (poll_expired(t0)) {
-                  atomicOr(sp.flags, SANTA_FLAG_SYNC_TIMEOUT);
-                  break;
-                }
-                v[r] = ld_strong_u64(sy.part + ((size_t)bh * CS + r) * D + d);
-              }
-              s += __uint_as_float((uint32_t)v[r]);  // fixed split order
-            }
-            store_out<T, D>(sp, (size_t)bh, d, s * invS);
-          }
-        }
-      }
-      if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 6);
-      group_bar();  // sPart / sTicket are rewritten by the next item
-      if (gtid == 0 && tslot >= 0) STEP_TRACE(tslot + 7);
-      it += grid;
-      ++ord;
-    }
+    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag8);
   }
   // ---------------- exit ticket: the last CTA out advances the epoch ----------------
   __syncthreads();

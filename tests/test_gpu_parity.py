@@ -50,14 +50,14 @@ def test_c1_fp32_single_head(mode):
     REPORT.append(("c1", mode, check_parity(inp, out, idx, 16, mode, 0x5A17A)))
 
 
-@pytest.mark.parametrize("path", ["step", "two_kernel"])
+@pytest.mark.parametrize("path", ["step", "step_tc", "two_kernel"])
 @pytest.mark.parametrize("mode", o.MODES)
 @pytest.mark.parametrize("paged", [False, True])
 def test_bf16_gqa_ragged(mode, paged, path):
     """Llama GQA shape (H=32, H_kv=8, d=128, bf16), ragged seqlens spanning many chunks and
     partial tails; contiguous and shuffled paged (P=64) layouts; both execution paths."""
     inp = si.make_decode_inputs(2, 32, 8, 128, [4097, 1000], dtype="bf16", seed=2,
-                                page_size=64 if paged else 0)
+                                page_size=(128 if path == "step_tc" else 64) if paged else 0)
     inp = to_cuda(inp)
     out, idx = gpu_decode(inp, 256, mode, seed=11, offset=3, paged=paged, path=path)
     REPORT.append(("gqa", mode, paged, path, check_parity(inp, out, idx, 256, mode, 11, 3)))
@@ -79,7 +79,7 @@ def test_peaked_workloads(workload):
         check_parity(inp, out, idx, 128, mode, 9)
 
 
-@pytest.mark.parametrize("path", ["step", "two_kernel"])
+@pytest.mark.parametrize("path", ["step", "step_tc", "two_kernel"])
 def test_edge_cases_small_and_large_budgets(path):
     # seqlen 1, S = 1, S > n (with replacement), non-power-of-two S, big max_seqlen padding
     inp = to_cuda(si.make_decode_inputs(3, 8, 2, 128, [1, 17, 300], dtype="bf16", seed=5))
@@ -98,7 +98,7 @@ def test_edge_cases_small_and_large_budgets(path):
     assert torch.equal(idx1, idx2) and torch.equal(out1, out2)
 
 
-@pytest.mark.parametrize("path", ["step", "two_kernel"])
+@pytest.mark.parametrize("path", ["step", "step_tc", "two_kernel"])
 def test_empty_sequence_sets_flag_and_zeroes(path):
     inp = to_cuda(si.make_decode_inputs(2, 8, 2, 128, [5, 40], dtype="bf16", seed=6))
     inp.seqlens[0] = 0
@@ -172,6 +172,10 @@ def test_full_size_config2_sampled_heads():
     inp = to_cuda(si.make_decode_inputs(1, 32, 8, 128, 32768, dtype="bf16", seed=0))
     out, idx = gpu_decode(inp, 256, "stratified", seed=0x5A17A, path="step")
     out2, idx2 = gpu_decode(inp, 256, "stratified", seed=0x5A17A, path="two_kernel")
+    out3, idx3 = gpu_decode(inp, 256, "stratified", seed=0x5A17A, path="step_tc")
+    # the tensor-core score stage sums the same bf16 products in another order (fp32): same indices
+    # up to threshold-at-boundary cases
+    assert (idx != idx3).float().mean().item() < 1e-3
     # the paths differ only in the in-chunk prefix encoding (fp32 vs 24-bit fixed point, reading #23):
     # indices may differ only where a threshold lies within ~2^-24 of a key boundary
     assert (idx != idx2).float().mean().item() < 1e-3
@@ -179,7 +183,7 @@ def test_full_size_config2_sampled_heads():
         sub = si.DecodeInputs(q=inp.q[:, 4 * kvh:4 * kvh + 4].contiguous(), K=inp.K[:, kvh:kvh + 1].contiguous(),
                               V=inp.V[:, kvh:kvh + 1].contiguous(), seqlens=inp.seqlens, n_heads=4, n_kv_heads=1,
                               head_dim=128, dtype="bf16")
-        for path, o_, i_ in (("step", out, idx), ("two_kernel", out2, idx2)):
+        for path, o_, i_ in (("step", out, idx), ("two_kernel", out2, idx2), ("step_tc", out3, idx3)):
             REPORT.append(("c2-full", kvh, path,
                            check_parity(sub, o_[:, 4 * kvh:4 * kvh + 4], i_[:, 4 * kvh:4 * kvh + 4], 256, "stratified",
                                         0x5A17A, head_offset=4 * kvh)))

@@ -26,7 +26,7 @@ def main():
         ws = santa.workspace(probs[0][1], S, "cuda")
         st = torch.cuda.current_stream()
         row = {}
-        for path in ("step", "two_kernel"):
+        for path in ("step", "step_tc", "two_kernel"):
             def f(i):
                 inp, geo, out = probs[i % NR]
                 santa.santa_decode_attention_path(geo, inp.q, inp.K, inp.V, inp.seqlens, S, "stratified", 7, i, out,
@@ -43,6 +43,7 @@ def main():
             torch.cuda.synchronize()
             row[path] = round(e0.elapsed_time(e1) / K * 1e3, 2)
         row["speedup_step"] = round(row["two_kernel"] / row["step"], 3)
+        row["speedup_step_tc"] = round(row["two_kernel"] / row["step_tc"], 3)
         res[B] = row
         del probs, ws
         torch.cuda.empty_cache()
