@@ -129,8 +129,10 @@ size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
  * Execution: for bf16/fp16 caches (contiguous, or pages of a multiple of 64
  * tokens) and max_seqlen <= 65536 the whole step is ONE cooperative persistent launch (the step
  * kernel: interleaved TMA score stream; each (b, kv-head) unit is sampled as soon as its chunks are
- * scored, chunk results published as tagged words -- no fences); otherwise the split-KV score pass
- * + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
+ * scored, chunk results published as tagged words -- no fences); from 256 query heads per call
+ * (batch * n_heads) with S <= 256 its score stage runs on tcgen05 tensor cores (TMEM
+ * accumulators); otherwise
+ * the split-KV score pass + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
  * in-chunk prefixes are fp32 (two-kernel) vs 24-bit fixed point (step kernel, DESIGN.md reading
  * #23), so an index may differ only where a threshold lies within ~2^-24 of a key boundary. */
 santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,

@@ -25,6 +25,8 @@ namespace {
 // and the score pass + PDL-chained sampler pair (fp32 caches, page sizes not a multiple of 64,
 // contexts > 64k, profiling, and the sequence-sharded phases).
 
+constexpr int kTcMinHeads = 256;  // AUTO switches the step kernel's score stage to tcgen05 from here
+
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -717,8 +719,16 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   // AUTO = the single-launch step kernel when eligible (measured >= the two-kernel path at every
   // batch size of config 3, tools/path_sweep.py)
   if (!a.events && path != SANTA_PATH_TWO_KERNEL) {
-    a.tensor_core = path == SANTA_PATH_STEP_TC;
+    // AUTO: the tensor-core score stage from 256 query heads per call and S <= 256 (measured:
+    // faster from batch 8 at H = 32; at S = 512 its 448-thread CTA leaves the sampler group too few
+    // registers and the sampling, not the stream, bounds the step -- profiles/r01_v5_path_sweep.json)
+    a.tensor_core = path == SANTA_PATH_STEP_TC ||
+                    (path == SANTA_PATH_AUTO && (int64_t)g->batch * g->n_heads >= kTcMinHeads && S <= 256);
     s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
+    if (s == SANTA_ERR_UNSUPPORTED && path == SANTA_PATH_AUTO && a.tensor_core) {
+      a.tensor_core = false;  // e.g. pages not a multiple of 128 tokens
+      s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
+    }
     if (s == SANTA_OK) return last_cuda();
     if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL || path == SANTA_PATH_STEP_TC) return s;
   }

@@ -188,7 +188,7 @@ __device__ __forceinline__ void warp_chunk_epilogue_ll(const float* sS, int n_va
 // Sampler-group item: (b, h, split rank of CS), 64-key chunks.  Arithmetic as sample_item
 // (readings #1-#5, #21) except the in-chunk search, which runs on the 24-bit fixed-point prefix
 // (reading #23).  Returns the partial sum (not yet x 1/S) in sPart[D].
-template <typename T, int D, int G>
+template <typename T, int D, int G, int U = 8>
 __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, int b, int h, int rank, int CS,
                                    unsigned char* smem, int tslot, uint32_t tag32, uint32_t tag8, bool dry) {
   constexpr int NT = kStepSamplers * 32, NW = kStepSamplers, NHW = NT / 16;
@@ -350,7 +350,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   constexpr int VCH = D * EB / 16;
   constexpr int NCH = (VCH + 15) / 16;
   constexpr int EPC = 16 / EB;
-  constexpr int U = 8;  // samples in flight per half-warp (8 half-warps x 8 = 64 strata per round)
+  // U samples in flight per half-warp (8 half-warps x U strata per round)
   const int hw = tid >> 4, l = tid & 15;
   const unsigned hmask = 0xffffu << (tid & 16);
   float acc[NCH][EPC];
@@ -472,7 +472,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
 
 // The sampler-group work loop (items it = blockIdx.x + k * grid), shared by the step kernels.
 // Sampler warps are the LAST NSW warps of the CTA.
-template <typename T, int D, int G, int NSW>
+template <typename T, int D, int G, int NSW, int U = 8>
 __device__ __forceinline__ void step_sampler_loop(const SampleParams& sp, const StepSync& sy, unsigned char* samp_smem,
                                                   uint32_t tag32, uint32_t tag8) {
   const int grid = gridDim.x;
@@ -485,7 +485,7 @@ __device__ __forceinline__ void step_sampler_loop(const SampleParams& sp, const 
     const int rank = it % CS, bh = it / CS;
     const int b = bh / sp.H, h = bh - b * sp.H;
     const int tslot = (sy.trace && ord < 3) ? 24 + 10 * ord : -1;
-    const float* sPart = step_sample_item<T, D, G>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
+    const float* sPart = step_sample_item<T, D, G, U>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
     if (CS == 1) {
       for (int d = gtid; d < D; d += NSW * 32) store_out<T, D>(sp, (size_t)bh, d, sPart[d] * invS);
     } else {

@@ -273,7 +273,9 @@ __global__ void __launch_bounds__(32 * (kTcEGWarps + 2 + NSW), 1)
     if (lane == 0 && sy.trace) STEP_TRACE(2 + warp);
   } else {
     // ---------------- sampler group ----------------
-    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag8);
+    // 4 samples in flight per half-warp: this kernel serves large batches (many rounds per item
+    // anyway) and must fit 448 threads x 128 registers without spilling
+    step_sampler_loop<T, D, G, NSW, 4>(sp, sy, samp_smem, tag32, tag8);
   }
   // ---------------- teardown: TMEM, then the exit ticket (the last CTA out advances the epoch) ----
   tc_fence_before();

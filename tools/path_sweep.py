@@ -14,8 +14,9 @@ import santa_inputs as si  # noqa: E402
 
 def main():
     res = {}
-    S, n = 256, 32768
-    for B in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8,16,32").split(",")]:
+    n = 32768
+    Ss = [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "256").split(",")]
+    for B, S in [(int(x), S) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8,16,32").split(",") for S in Ss]:
         prob = 2 * B * 8 * n * 128 * 2
         NR = max(1, -(-(512 << 20) // prob))
         probs = []
@@ -44,7 +45,7 @@ def main():
             row[path] = round(e0.elapsed_time(e1) / K * 1e3, 2)
         row["speedup_step"] = round(row["two_kernel"] / row["step"], 3)
         row["speedup_step_tc"] = round(row["two_kernel"] / row["step_tc"], 3)
-        res[B] = row
+        res[f"B{B}_S{S}"] = row
         del probs, ws
         torch.cuda.empty_cache()
     print(json.dumps(res))
