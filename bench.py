@@ -69,12 +69,14 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic():
-    """dram bytes per launch of the dominant (step) kernel from the committed ncu --set full summary."""
+def load_traffic(path="two_kernel"):
+    """dram bytes per launch of the dominant kernel of `path` from the committed ncu --set full
+    summaries (profiles/dominant_kernel_ncu.json, config 2)."""
     p = os.path.join(ROOT, "profiles", "dominant_kernel_ncu.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("dram_bytes_per_launch")
+            d = json.load(open(p))
+            return d.get(path, {}).get("dram_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -498,34 +500,15 @@ def main():
         "pct_of_peak": {"measured_copy": round(100 * value / world / peak, 1),
                         "spec_8TBps": round(100 * value / world / 8000.0, 1)},
         "clocks": clk.summary(),
-        # one santa_step_kernel launch per step (score pass + sampler kernel when not eligible)
-        "gpu_launches": args.steps * (1 if (args.page_size % 64 == 0 and args.seqlen <= 65536) else 2),
+        # score pass + sampler kernel per step on the two-kernel path, one launch on the step kernels
+        "gpu_launches": args.steps * (2 if santa.santa_auto_path(probs[0].geo, args.S) == "two_kernel" else 1),
         "paper_context": PAPER_CONTEXT,
     }
 
-    step_kernel = args.page_size % 64 == 0 and args.seqlen <= 65536  # santa_decode_attention's AUTO path
+    auto = santa.santa_auto_path(probs[0].geo, args.S)  # the path santa_decode_attention takes
+    res["path"] = auto
     if not args.no_extras:
-        # (1) the dominant kernel = the step kernel itself (one launch per step): its per-launch time is
-        # the timed loop above, measured with CUDA events on the launching stream
-        achieved = bytes_step / (ms * 1e-3) / 1e9
-        res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                           "frac": round(achieved / peak, 4), "traffic": load_traffic(),
-                           "kernel": ("santa_step_kernel<bf16,128,4,6,2,4> (whole step: score stream + sampling)"
-                                      if step_kernel else "score_stream_kernel + sample_gather_kernel"),
-                           "peak_source": peak_src,
-                           "algorithmic_bytes_per_launch": bytes_step,
-                           "kernel_us": round(ms * 1e3, 2),
-                           "timing": "back-to-back launches over rotating KV caches > 4x L2, CUDA events",
-                           "share_of_step": 1.0 if step_kernel else None}
-        # (1b) the two-kernel path and its phases (the score pass is the streaming half of the step)
-        def step2(i):
-            p = probs[i % NR]
-            santa.santa_decode_attention_path(p.geo, p.q, p.K, p.V, p.seqlens, args.S, args.mode, args.seed, i,
-                                              p.out, None, ws, "two_kernel", stream)
-        for i in range(args.warmup):
-            step2(i)
-        t2ms = max_over_ranks(timed_loop(step2, args.steps))
-
+        # the score pass alone (the streaming half of the two-kernel path), back-to-back
         def score(i):
             p = probs[i % NR]
             santa.santa_score_phase(p.geo, p.q, p.K, p.seqlens, ws, stream)
@@ -540,13 +523,42 @@ def main():
                                      stream)
         sgms = max_over_ranks(timed_loop(sample, args.steps))
         sach = (kb + B * H * d * 2) / (sms * 1e-3) / 1e9
-        res["two_kernel_path"] = {
-            "us_per_step": round(t2ms * 1e3, 2), "GBps": round(bytes_step / (t2ms * 1e-3) / 1e9, 1),
-            "score_phase": {"kernel": "score_stream_kernel<bf16,128,4,6,2>", "us": round(sms * 1e3, 2),
-                            "achieved_GBps": round(sach, 1), "frac": round(sach / peak, 4),
-                            "algorithmic_bytes": kb + B * H * d * 2},
-            "sample_phase_us": round(sgms * 1e3, 2),
-            "step_kernel_speedup": round(t2ms / ms, 3)}
+        # (1) the dominant kernel of the AUTO path: the score pass (two-kernel path) or the step
+        # kernel itself (one launch per step); CUDA events on the launching stream
+        if auto == "two_kernel":
+            res["roofline"] = {"bound": "hbm", "achieved": round(sach, 1), "peak": peak, "unit": "GB/s",
+                               "frac": round(sach / peak, 4), "traffic": load_traffic(auto),
+                               "kernel": "score_stream_kernel<bf16,128,4,6,2> (split-KV score pass, interleaved)",
+                               "peak_source": peak_src, "algorithmic_bytes_per_launch": kb + B * H * d * 2,
+                               "kernel_us": round(sms * 1e3, 2),
+                               "timing": "the pass alone, back-to-back over rotating KV caches > 4x L2, CUDA events",
+                               "sample_phase_us": round(sgms * 1e3, 2), "share_of_step": round(sms / ms, 3)}
+        else:
+            achieved = bytes_step / (ms * 1e-3) / 1e9
+            res["roofline"] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                               "frac": round(achieved / peak, 4), "traffic": load_traffic(auto),
+                               "kernel": f"santa_{auto}_kernel (whole step in one launch)", "peak_source": peak_src,
+                               "algorithmic_bytes_per_launch": bytes_step, "kernel_us": round(ms * 1e3, 2),
+                               "timing": "back-to-back launches over rotating KV caches > 4x L2, CUDA events",
+                               "share_of_step": 1.0}
+        # (1b) every execution path on the same protocol
+        paths = {}
+        for pth in ("two_kernel", "step", "step_tc"):
+            def stepp(i, pth=pth):
+                p = probs[i % NR]
+                santa.santa_decode_attention_path(p.geo, p.q, p.K, p.V, p.seqlens, args.S, args.mode, args.seed, i,
+                                                  p.out, None, ws, pth, stream)
+            try:
+                for i in range(args.warmup):
+                    stepp(i)
+                t = max_over_ranks(timed_loop(stepp, args.steps))
+                paths[pth] = {"us_per_step": round(t * 1e3, 2), "GBps": round(bytes_step / (t * 1e-3) / 1e9, 1)}
+            except Exception as ex:  # noqa: BLE001 -- a path not eligible for this geometry
+                paths[pth] = f"unavailable: {ex}"[:120]
+        paths["score_phase"] = {"kernel": "score_stream_kernel<bf16,128,4,6,2>", "us": round(sms * 1e3, 2),
+                                "achieved_GBps": round(sach, 1), "frac": round(sach / peak, 4)}
+        paths["sample_phase_us"] = round(sgms * 1e3, 2)
+        res["paths"] = paths
         # (2) isolated single-step latency, the paper's protocol (flush write before each step)
         iso = []
         for i in range(args.steps):

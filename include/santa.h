@@ -78,8 +78,8 @@ typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q,
                                         /* (see santa_workspace_bytes); outputs are invalid        */
 
 typedef enum {
-  SANTA_PATH_AUTO = 0,        /* the step kernel when eligible, else the two-kernel path          */
-  SANTA_PATH_STEP_KERNEL = 1, /* force the single launch (SANTA_ERR_UNSUPPORTED if not eligible) */
+  SANTA_PATH_AUTO = 0,        /* santa_auto_path's choice                                         */
+  SANTA_PATH_STEP_KERNEL = 1, /* the single launch, mma.sync score stage (ERR_UNSUPPORTED if not eligible) */
   SANTA_PATH_TWO_KERNEL = 2,  /* score pass + PDL-chained sampler kernel                          */
   SANTA_PATH_STEP_TC = 3      /* the step kernel with its score stage on tcgen05 tensor cores    */
 } santa_path;
@@ -126,13 +126,12 @@ size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
  *   sampling is with replacement), out [B,H,d] (same dtype as q),
  *   idx_out: NULL or int32 [B,H,S] receiving J_m (token ids within the sequence).
  * Only the LOW 32 bits of `offset` enter the Philox counter.
- * Execution: for bf16/fp16 caches (contiguous, or pages of a multiple of 64
- * tokens) and max_seqlen <= 65536 the whole step is ONE cooperative persistent launch (the step
- * kernel: interleaved TMA score stream; each (b, kv-head) unit is sampled as soon as its chunks are
- * scored, chunk results published as tagged words -- no fences); from 256 query heads per call
- * (batch * n_heads) with S <= 256 its score stage runs on tcgen05 tensor cores (TMEM
- * accumulators); otherwise
- * the split-KV score pass + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
+ * Execution (santa_auto_path reports the choice): from 1024 query heads per
+ * call (batch * n_heads) with S <= 256, bf16/fp16, max_seqlen <= 65536 and contiguous or
+ * 128-multiple pages, the whole step is ONE cooperative persistent launch (the tcgen05 step kernel:
+ * interleaved TMA score stream, score stage on tensor cores with TMEM accumulators, each
+ * (b, kv-head) unit sampled as soon as its chunks are scored, chunk results published as tagged
+ * words -- no fences); otherwise the split-KV score pass + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
  * in-chunk prefixes are fp32 (two-kernel) vs 24-bit fixed point (step kernel, DESIGN.md reading
  * #23), so an index may differ only where a threshold lies within ~2^-24 of a key boundary. */
 santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,
@@ -152,6 +151,10 @@ santa_status santa_decode_attention_profiled(const santa_geometry* geo, const vo
                                              int32_t* idx_out, void* workspace,
                                              size_t workspace_bytes, void* const* events,
                                              void* stream);
+
+/* The execution path santa_decode_attention (AUTO) takes for this geometry and budget
+ * (a santa_path value; -1 if the geometry is invalid).  Pure host logic. */
+int32_t santa_auto_path(const santa_geometry* geo, int32_t S);
 
 /* santa_decode_attention with an explicit execution path (santa_path); AUTO is exactly
  * santa_decode_attention.  Used by the tests and bench.py to compare the two paths. */

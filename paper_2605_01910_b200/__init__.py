@@ -19,7 +19,7 @@ from . import _abi
 from ._abi import DTYPES, FLAG_EMPTY_SEQ, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry, SantaError
 
 __all__ = [
-    "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes",
+    "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes", "santa_auto_path",
     "santa_decode_attention", "santa_decode_attention_path", "santa_decode_attention_profiled", "santa_score_phase",
     "santa_sample_phase", "PATHS", "FLAG_SYNC_TIMEOUT",
     "santa_dense_reference",
@@ -69,6 +69,14 @@ def santa_version() -> str:
 
 def santa_workspace_bytes(geo: Geometry, S: int) -> int:
     return int(_abi.LIB.santa_workspace_bytes(ctypes.byref(geo), S))
+
+
+def santa_auto_path(geo: Geometry, S: int) -> str:
+    """The execution path santa_decode_attention takes ("two_kernel", "step" or "step_tc")."""
+    code = int(_abi.LIB.santa_auto_path(ctypes.byref(geo), S))
+    if code < 0:
+        raise SantaError("santa_auto_path", 1)
+    return {v: k for k, v in PATHS.items()}[code]
 
 
 def workspace(geo: Geometry, S: int, device="cuda") -> torch.Tensor:

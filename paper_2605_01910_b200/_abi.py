@@ -54,6 +54,7 @@ def _load() -> ctypes.CDLL:
         "santa_status_string": ([i32], ctypes.c_char_p),
         "santa_version": ([], ctypes.c_char_p),
         "santa_workspace_bytes": ([G, i32], sz),
+        "santa_auto_path": ([G, i32], i32),
         "santa_decode_attention": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_decode_attention_path": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, i32, vp], i32),
         "santa_decode_attention_profiled": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp, vp], i32),

@@ -25,7 +25,7 @@ namespace {
 // and the score pass + PDL-chained sampler pair (fp32 caches, page sizes not a multiple of 64,
 // contexts > 64k, profiling, and the sequence-sharded phases).
 
-constexpr int kTcMinHeads = 256;  // AUTO switches the step kernel's score stage to tcgen05 from here
+constexpr int kTcMinHeads = 1024;  // AUTO runs the tcgen05 step kernel from here (and S <= 256)
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -697,12 +697,20 @@ santa_status validate_bern(const santa_geometry* g, const void* q, const void* K
   return SANTA_OK;
 }
 
+int auto_path(const santa_geometry* g, int S) {
+  const bool step_ok = g->dtype != SANTA_F32 && g->max_seqlen <= 65536 &&
+                       (!g->page_table || g->page_size % kTcTileKeys == 0);
+  if (step_ok && (int64_t)g->batch * g->n_heads >= kTcMinHeads && S <= 256) return SANTA_PATH_STEP_TC;
+  return SANTA_PATH_TWO_KERNEL;
+}
+
 santa_status decode_common(const santa_geometry* g, const void* q, const void* K, const void* V,
                            const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
                            void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
                            void* stream, int path = SANTA_PATH_AUTO) {
   santa_status s = validate_geometry(g);
   if (path < SANTA_PATH_AUTO || path > SANTA_PATH_STEP_TC) return SANTA_ERR_INVALID_ARG;
+  const bool auto_requested = path == SANTA_PATH_AUTO;
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
   if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
@@ -718,19 +726,20 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   const int G = g->n_heads / g->n_kv_heads;
   // AUTO = the single-launch step kernel when eligible (measured >= the two-kernel path at every
   // batch size of config 3, tools/path_sweep.py)
+  // AUTO (measured, tools/path_sweep.py -> profiles/r01_v6_path_sweep.json): the tcgen05 step kernel
+  // from 1024 query heads per call with S <= 256 (batch 32: 391 vs 403 us); below that, the score
+  // pass + PDL-chained sampler (batch 1: 25.0 vs 26.8 us for the mma.sync step kernel) -- the
+  // sampler kernel then has every SM for the final sampling chain
+  if (path == SANTA_PATH_AUTO) path = auto_path(g, S);
   if (!a.events && path != SANTA_PATH_TWO_KERNEL) {
-    // AUTO: the tensor-core score stage from 256 query heads per call and S <= 256 (measured:
-    // faster from batch 8 at H = 32; at S = 512 its 448-thread CTA leaves the sampler group too few
-    // registers and the sampling, not the stream, bounds the step -- profiles/r01_v5_path_sweep.json)
-    a.tensor_core = path == SANTA_PATH_STEP_TC ||
-                    (path == SANTA_PATH_AUTO && (int64_t)g->batch * g->n_heads >= kTcMinHeads && S <= 256);
+    a.tensor_core = path == SANTA_PATH_STEP_TC;
     s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
-    if (s == SANTA_ERR_UNSUPPORTED && path == SANTA_PATH_AUTO && a.tensor_core) {
+    if (s == SANTA_ERR_UNSUPPORTED && a.tensor_core && auto_requested) {
       a.tensor_core = false;  // e.g. pages not a multiple of 128 tokens
       s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
     }
     if (s == SANTA_OK) return last_cuda();
-    if (s != SANTA_ERR_UNSUPPORTED || path == SANTA_PATH_STEP_KERNEL || path == SANTA_PATH_STEP_TC) return s;
+    if (s != SANTA_ERR_UNSUPPORTED || !auto_requested) return s;
   }
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
@@ -758,6 +767,11 @@ const char* santa_status_string(santa_status s) {
 
 const char* santa_version(void) {
   return "libsanta 0.2 sm_100a (score_stream: TMA 128B-swizzle ring + mma.sync m16n8k16, persistent; score_chunk fallback; sample_gather per (b,h); dense_partial+combine; bernoulli)";
+}
+
+int32_t santa_auto_path(const santa_geometry* g, int32_t S) {
+  if (validate_geometry(g) != SANTA_OK || S < 1) return -1;
+  return auto_path(g, S);
 }
 
 size_t santa_workspace_bytes(const santa_geometry* g, int32_t S) {

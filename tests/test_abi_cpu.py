@@ -100,3 +100,15 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|santa_oracle|oracle\.", txt, re.M), f
+
+
+def test_auto_path_policy_is_host_logic():
+    """santa_auto_path (pure host arithmetic): the two-kernel path below 1024 query heads or for
+    S > 256 / fp32 / long contexts; the tcgen05 step kernel from 1024 heads with S <= 256."""
+    assert santa.santa_auto_path(_geo(), 256) == "two_kernel"             # config 2
+    assert santa.santa_auto_path(_geo(batch=32), 256) == "step_tc"        # config 3
+    assert santa.santa_auto_path(_geo(batch=32), 512) == "two_kernel"
+    assert santa.santa_auto_path(_geo(batch=32, dtype=1), 256) == "two_kernel"   # fp32 cache
+    assert santa.santa_auto_path(_geo(batch=32, max_seqlen=131072), 256) == "two_kernel"
+    with pytest.raises(santa.SantaError):
+        santa.santa_auto_path(_geo(max_seqlen=0), 256)
