@@ -43,6 +43,13 @@ __device__ __forceinline__ uint4 ldg_nc(const void* p) {
   return r;
 }
 
+// plain weak 128-bit global load (L1-allocating)
+__device__ __forceinline__ uint4 ldg_plain(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+
 __device__ __forceinline__ float4 ldcg_f4(const void* p) {
   float4 r;
   asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));

@@ -284,6 +284,12 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
     for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
   const T* Vb = reinterpret_cast<const T*>(p.V);
   const float* Pbase = p.stash + bh * p.stash_stride;
+  // V row address: contiguous caches hoist the (b, kv-head) base (one multiply-add per row; the
+  // generic paged/contiguous KvLayout::row() inlined per sample serialised the loads' issue)
+  const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
+  auto vrow = [&](int t) -> const T* {
+    return p.kv.page_table ? Vb + p.kv.row(b, kvh, t, D) : vbase + (int64_t)t * D;
+  };
   const int tok0 = p.token_offset ? __ldg(p.token_offset + b) : 0;
   // warp-uniform trip count: warp w walks sample pairs 2w, 2w+1 (+ NHW per u); the full-mask
   // ballots below must be reached by both half-warps
@@ -303,37 +309,52 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      // warp-uniform: both half-warps execute every ballot with the full mask; inactive samples
-      // have pv = +inf and tf = -inf, i.e. count 0
+      // in-chunk index k = min{k : P[k] > tf} = #{k : P[k] <= tf} (P non-decreasing; inactive samples
+      // and keys beyond the sequence load P = +inf).  L = 64, branch-free: one ballot over every
+      // lane's last value (lane j holds keys 4j..4j+3) + the crossing lane's own count.
       const int m = m0 + u * NHW;
-      const float tf = (cc[u] >= 0) ? sTl[m] : -INFINITY;
+      const bool on = cc[u] >= 0;
+      const float tf = on ? sTl[m] : -INFINITY;
       const float4 v = pv[u];
-      int k = __popc(__ballot_sync(0xffffffffu, v.x <= tf) & hmask) +
-              __popc(__ballot_sync(0xffffffffu, v.y <= tf) & hmask) +
-              __popc(__ballot_sync(0xffffffffu, v.z <= tf) & hmask) +
-              __popc(__ballot_sync(0xffffffffu, v.w <= tf) & hmask);
-      jj[u] = -1;
-      if (cc[u] >= 0) {
-        const float* P = Pbase + (size_t)cc[u] * p.L;
-        if (p.L != 64) k = thread_chunk_search(P, nn[u], tf);
-        if (k >= nn[u]) {  // rounding: threshold at/after the chunk total -> the last positive-mass key
-          const float tot = __ldcg(P + nn[u] - 1);
-          k = thread_chunk_search(P, nn[u], nextafterf(tot, -INFINITY));
+      int k;
+      if (p.L == 64) {
+        const int full_lanes = __popc(__ballot_sync(0xffffffffu, v.w <= tf) & hmask);
+        const int own = (v.x <= tf) + (v.y <= tf) + (v.z <= tf) + (v.w <= tf);
+        const int cross = __shfl_sync(0xffffffffu, own, (tid & 16) + min(full_lanes, 15));
+        k = full_lanes < 16 ? 4 * full_lanes + cross : 64;
+        // rounding put tf at/after the chunk's total: the first key reaching the total (the last
+        // positive-mass key); the total P[n-1] sits in lane (n-1)/4, component (n-1)%4
+        if (__any_sync(0xffffffffu, on && k >= nn[u])) {
+          const int ln = max(nn[u] - 1, 0);
+          const int src = (tid & 16) + (ln >> 2);
+          const float tx = __shfl_sync(0xffffffffu, v.x, src), ty = __shfl_sync(0xffffffffu, v.y, src);
+          const float tz = __shfl_sync(0xffffffffu, v.z, src), tw = __shfl_sync(0xffffffffu, v.w, src);
+          const float tot = (ln & 3) == 0 ? tx : (ln & 3) == 1 ? ty : (ln & 3) == 2 ? tz : tw;
+          const int fl2 = __popc(__ballot_sync(0xffffffffu, v.w < tot) & hmask);
+          const int own2 = (v.x < tot) + (v.y < tot) + (v.z < tot) + (v.w < tot);
+          const int cross2 = __shfl_sync(0xffffffffu, own2, (tid & 16) + min(fl2, 15));
+          if (on && k >= nn[u]) k = fl2 < 16 ? 4 * fl2 + cross2 : nn[u] - 1;
         }
-        jj[u] = cc[u] * p.L + k;
-        if (l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u] + tok0;
-      } else if (m < Sl && l == 0 && p.idx_out) {
-        p.idx_out[bh * S + m_lo + m] = -1;  // stratum owned by another sequence shard
+      } else {
+        k = 0;
+        if (on) {
+          const float* P = Pbase + (size_t)cc[u] * p.L;
+          k = thread_chunk_search(P, nn[u], tf);
+          if (k >= nn[u]) k = thread_chunk_search(P, nn[u], nextafterf(__ldcg(P + nn[u] - 1), -INFINITY));
+        }
       }
+      jj[u] = on ? cc[u] * p.L + min(k, nn[u] - 1) : -1;
+      if (on && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u] + tok0;
+      if (!on && m < Sl && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = -1;  // another shard's stratum
     }
+    if (mw == 0) SANTA_TRACE(8);  // indices known (stash loaded, ballots done)
     uint4 raw[U][NCH];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int q = 0; q < NCH; ++q) {
         const int ch = l + 16 * q;
-        raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(Vb + p.kv.row(b, kvh, jj[u], D) + ch * EPC)
-                                             : make_uint4(0u, 0u, 0u, 0u);
+        raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(vrow(jj[u]) + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -354,6 +375,7 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
         }
       }
   }
+  SANTA_TRACE(9);  // V rows gathered and added (thread 0)
   // deterministic reduction over the half-warps (fixed order)
 #pragma unroll
   for (int q = 0; q < NCH; ++q) {

@@ -360,6 +360,12 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
     for (int e = 0; e < EPC; ++e) acc[qq][e] = 0.f;
   const T* Vb = reinterpret_cast<const T*>(p.V);
   const uint32_t* Qbase = sy.stash + bh * (size_t)p.Cmax * 64;
+  // V row address: contiguous caches hoist the (b, kv-head) base (one multiply-add per row; the
+  // generic paged/contiguous KvLayout::row() inlined per sample serialised the loads' issue)
+  const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
+  auto vrow = [&](int t) -> const T* {
+    return p.kv.page_table ? Vb + p.kv.row(b, kvh, t, D) : vbase + (int64_t)t * D;
+  };
   const uint32_t tg = tag8 << 24;
   for (int mw = 2 * wg; mw < Sl; mw += NHW * U) {
     const int m0 = mw + (hw & 1);
@@ -430,8 +436,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
 #pragma unroll
       for (int qq = 0; qq < NCH; ++qq) {
         const int ch = l + 16 * qq;
-        raw[u][qq] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(Vb + p.kv.row(b, kvh, jj[u], D) + ch * EPC)
-                                              : make_uint4(0u, 0u, 0u, 0u);
+        raw[u][qq] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(vrow(jj[u]) + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
     for (int u = 0; u < U; ++u)

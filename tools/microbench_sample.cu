@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "fused_kernel_gridsync.cuh"
@@ -92,7 +93,7 @@ int main() {
   const size_t ssm = 1024 + (size_t)NW * G * L * 4 + (size_t)NW * SPW * (16384 + 16);
   auto skern = score_stream_kernel<bf16, 128, 4, NW, SPW>;
   cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-  const size_t psm = (size_t)Cmax * 16 + (size_t)S * 16 + 17 * 128 * 4 + 64;
+  const size_t psm = getenv("PAD") ? (size_t)120 * 1024 : (size_t)Cmax * 16 + (size_t)S * 16 + 17 * 128 * 4 + 64;
   auto pkern = sample_gather_kernel<bf16, 128, 4>;
   cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
   auto launch_pdl = [&](SampleParams p) {
@@ -212,6 +213,19 @@ int main() {
         for (int i = 0; i < 7; ++i) ph[i].push_back((double)(h[c * 16 + i + 1] - h[c * 16 + i]));
     }
     printf("---- %s ----\n", mode == 0 ? "score -> sample (PDL)" : mode == 1 ? "score; sync; sample" : "sample only (stash hot)");
+    {
+      std::vector<double> a, b2, c2;
+      for (int c = 0; c < B * H; ++c) {
+        if (!h[c * 16 + 8] || !h[c * 16 + 9]) continue;
+        a.push_back((double)(h[c * 16 + 8] - h[c * 16 + 5]));
+        b2.push_back((double)(h[c * 16 + 9] - h[c * 16 + 8]));
+        c2.push_back((double)(h[c * 16 + 6] - h[c * 16 + 9]));
+      }
+      std::sort(a.begin(), a.end()); std::sort(b2.begin(), b2.end()); std::sort(c2.begin(), c2.end());
+      if (!a.empty())
+        printf("  (last rep) stash+ballots %6.0f ns | V gather+add %6.0f ns | reduce barrier %6.0f ns (medians)\n",
+               a[a.size() / 2], b2[b2.size() / 2], c2[c2.size() / 2]);
+    }
     for (int i = 0; i < 7; ++i) {
       std::sort(ph[i].begin(), ph[i].end());
       printf("phase %-22s median %8.0f ns   p90 %8.0f ns\n", names[i], ph[i][ph[i].size() / 2],
