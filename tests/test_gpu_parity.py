@@ -63,11 +63,19 @@ def test_bf16_gqa_ragged(mode, paged, path):
     REPORT.append(("gqa", mode, paged, path, check_parity(inp, out, idx, 256, mode, 11, 3)))
 
 
+@pytest.mark.parametrize("path", ["auto", "step", "step_tc"])
 @pytest.mark.parametrize("dtype,d,H,Hkv", [("f16", 64, 16, 2), ("bf16", 64, 8, 8), ("bf16", 128, 8, 4),
-                                            ("f32", 128, 16, 8), ("bf16", 128, 4, 2)])
-def test_dtype_shape_variants(dtype, d, H, Hkv):
+                                            ("f32", 128, 16, 8), ("bf16", 128, 4, 2), ("f16", 128, 32, 4)])
+def test_dtype_shape_variants(dtype, d, H, Hkv, path):
+    """dtypes, head dims and GQA group sizes G = 8, 1, 2, 2, 8 on every decode path (the step
+    kernels take bf16/fp16 only: fp32 must be refused, not silently rerouted)."""
     inp = to_cuda(si.make_decode_inputs(2, H, Hkv, d, [777, 2048], dtype=dtype, seed=3, workload="temp4"))
-    out, idx = gpu_decode(inp, 64, "systematic", seed=5)
+    if dtype == "f32" and path != "auto":
+        with pytest.raises(santa.SantaError) as e:
+            gpu_decode(inp, 64, "systematic", seed=5, path=path)
+        assert e.value.status == 5  # SANTA_ERR_UNSUPPORTED
+        return
+    out, idx = gpu_decode(inp, 64, "systematic", seed=5, path=path)
     check_parity(inp, out, idx, 64, "systematic", 5)
 
 
