@@ -88,9 +88,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   __syncthreads();
   pdl_launch_dependents();
 
+  // chunks interleaved over the grid (as the score pass): warp j of CTA i takes
+  // w = i + (j + NW t) * grid, t = 0, 1, ...
   const int total = p.B * p.Hkv * p.Cmax;
-  const int lo = (int)(((long long)total * blockIdx.x) / gridDim.x);
-  const int hi = (int)(((long long)total * (blockIdx.x + 1)) / gridDim.x);
+  const int grid = gridDim.x;
+  const int wstep = NW * grid;
+  const int step_u = wstep / p.Cmax, step_c = wstep - step_u * p.Cmax;
   if (warp == NW) {
     // ---------------- TMA producer (one lane), one cursor per consumer warp ----------------
     if (lane == 0) {
@@ -102,8 +105,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       int live = 0;
 #pragma unroll
       for (int j = 0; j < NW; ++j) {
-        w[j] = lo + j;
-        cw[j].init(w[j] < hi ? w[j] : lo, p.Cmax);
+        w[j] = blockIdx.x + j * grid;
+        cw[j].init(w[j] < total ? w[j] : 0, p.Cmax);
         s[j] = 0;
         nst[j] = -1;
         k[j] = 0;
@@ -112,18 +115,18 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         live = 0;
 #pragma unroll
         for (int j = 0; j < NW; ++j) {
-          while (w[j] < hi && nst[j] <= 0) {
+          while (w[j] < total && nst[j] <= 0) {
             if (nst[j] == 0) {
-              w[j] += NW;
-              cw[j].advance(NW, 0, p.Cmax);
+              w[j] += wstep;
+              cw[j].advance(step_c, step_u, p.Cmax);
             }
-            if (w[j] >= hi) break;
+            if (w[j] >= total) break;
             const int b = cw[j].unit / p.Hkv;
             const int n_valid = min(L, __ldg(p.seqlens + b) - cw[j].c * L);
             nst[j] = n_valid > 0 ? (n_valid + SK - 1) / SK : 0;
             s[j] = 0;
           }
-          if (w[j] >= hi) continue;
+          if (w[j] >= total) continue;
           ++live;
           const int slot = j * SPW + (k[j] % SPW);
           const uint32_t ph = (uint32_t)(k[j] / SPW) & 1u;
@@ -159,10 +162,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   int kk = 0, cur_unit = -1, seqlen = 0;
   uint4 qf[D / 64][2];
   ChunkWalk cw;
-  cw.init(lo + warp < hi ? lo + warp : lo, p.Cmax);
-  for (int w = lo + warp; w < hi; w += NW) {
+  const int w0 = blockIdx.x + warp * grid;
+  cw.init(w0 < total ? w0 : 0, p.Cmax);
+  for (int w = w0; w < total; w += wstep) {
     const int c = cw.c, unit = cw.unit;
-    cw.advance(NW, 0, p.Cmax);
+    cw.advance(step_c, step_u, p.Cmax);
     const int b = unit / p.Hkv, kvh = unit - b * p.Hkv;
     const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
     if (unit != cur_unit) {

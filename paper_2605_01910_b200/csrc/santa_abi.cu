@@ -766,7 +766,7 @@ const char* santa_status_string(santa_status s) {
 }
 
 const char* santa_version(void) {
-  return "libsanta 0.2 sm_100a (score_stream: TMA 128B-swizzle ring + mma.sync m16n8k16, persistent; score_chunk fallback; sample_gather per (b,h); dense_partial+combine; bernoulli)";
+  return "libsanta 0.3 sm_100a (santa_step_kernel: single-launch persistent step, tagged-word publication; santa_step_tc_kernel: tcgen05 score stage, TMEM accumulators; score_stream: TMA 128B-swizzle ring + mma.sync, interleaved; sample_gather: thread-block clusters; dense: TMA flash-decoding; bernoulli)";
 }
 
 int32_t santa_auto_path(const santa_geometry* g, int32_t S) {
