@@ -411,7 +411,7 @@ struct RunStep {
     if constexpr (sizeof(T) != 2) {
       return SANTA_ERR_UNSUPPORTED;
     } else {
-      constexpr int NSW = kStepSamplers, NT = 32 * (kTcEGWarps + 2 + NSW);
+      constexpr int NSW = kStepSamplers, NT = 32 * kTcWarps;
       if (a.g->page_table && a.g->page_size % kTcTileKeys != 0) return SANTA_ERR_UNSUPPORTED;
       const size_t smem = step_tc_score_smem_bytes(D, G) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
       if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;

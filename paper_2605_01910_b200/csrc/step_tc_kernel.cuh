@@ -15,8 +15,11 @@
 //               accumulator, writes scaled scores to shared memory; two warps then run the
 //               64-key chunk epilogue (max, exp2, prefix, tagged publication) for the tile's 2 chunks
 //   warp 8      TMA producer (one lane): K tile (4 boxes of 64 rows x 128 B) + q rows per stage
-//   warp 9      MMA issuer (one lane) and TMEM allocator (the warp)
-//   warps 10+   the sampler group (step_sampler_loop)
+//   warp 9      MMA issuer (one lane) and TMEM allocator (the warp); warps 10-11 idle
+//   warps 12-15 the sampler group (step_sampler_loop)
+// Registers are rebalanced per warpgroup with setmaxnreg (512 threads x 128 at launch): the
+// producer/MMA warpgroup drops to 56, the epilogue groups to 112, the sampler group grows to 200
+// (at 128 it spilled and needed 4-sample rounds; config 3, S = 512 was sampler-bound).
 // TMEM: 4 accumulator buffers x 16 columns (64 columns allocated).  Paged caches need pages of a
 // multiple of 128 tokens (a tile never straddles pages).
 #pragma once
@@ -32,6 +35,8 @@ constexpr int kTcStages = 5;      // smem ring stages (one tile each)
 constexpr int kTcBufs = 4;        // TMEM accumulator buffers
 constexpr int kTcCols = 64;       // TMEM columns allocated (kTcBufs * kTcN)
 constexpr int kTcEGWarps = 8;     // two epilogue groups of 4 warps
+constexpr int kTcWarps = 16;      // EG0, EG1, {producer, MMA, 2 idle}, samplers: 4 warpgroups
+constexpr int kTcSamplerWarp0 = 12;
 
 // ---- tcgen05 / TMEM PTX helpers (sm_100a) -------------------------------------------------
 // Shared-memory matrix descriptor, K-major, 128B swizzle (cute UMMA::SmemDescriptor): start
@@ -101,11 +106,17 @@ __host__ inline size_t step_tc_score_smem_bytes(int D, int G) {
   return 1024 + kTcStages * stage + (size_t)2 * 2 * G * 64 * 4 + (size_t)(2 * kTcStages + 2 * kTcBufs) * 8 + 64;
 }
 
+template <int N>
+__device__ __forceinline__ void setmaxnreg_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N)); }
+template <int N>
+__device__ __forceinline__ void setmaxnreg_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N)); }
+
 template <typename T, int D, int G, int NSW>
-__global__ void __launch_bounds__(32 * (kTcEGWarps + 2 + NSW), 1)
+__global__ void __launch_bounds__(32 * kTcWarps, 1)
     santa_step_tc_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmQ,
                          ScoreParams p, SampleParams sp, StepSync sy) {
   static_assert(sizeof(T) == 2 && G <= kTcN, "tensor-core score stage: bf16/fp16, G <= 16");
+  static_assert(NSW == 4 && kTcSamplerWarp0 + NSW == kTcWarps, "the sampler group is the last warpgroup");
   constexpr int HALVES = D / 64;
   constexpr int kKBytes = HALVES * kTcTileKeys * 128;  // K tile: [half][128 rows][128 B]
   constexpr int kQBytes = HALVES * kTcN * 128;         // q rows: [half][16 rows][128 B]
@@ -170,6 +181,9 @@ __global__ void __launch_bounds__(32 * (kTcEGWarps + 2 + NSW), 1)
     return min(kTcTileKeys, __ldg(p.seqlens + b) - c2 * kTcTileKeys);
   };
 
+  // per-warpgroup register budgets (each role's code starts with its own setmaxnreg so ptxas
+  // allocates it under that budget): 2 x 4 x 112 + 4 x 56 + 4 x 200 = 1920 x 32 <= 64K registers
+  if (warp >= kTcEGWarps && warp < kTcSamplerWarp0) setmaxnreg_dec<56>();
   if (warp == kTcEGWarps) {
     // ---------------- TMA producer (one lane) ----------------
     if (lane == 0) {
@@ -231,6 +245,7 @@ __global__ void __launch_bounds__(32 * (kTcEGWarps + 2 + NSW), 1)
     __syncwarp();
   } else if (warp < kTcEGWarps) {
     // ---------------- epilogue groups ----------------
+    setmaxnreg_dec<112>();
     const int e = warp >> 2, wq = warp & 3;
     float* sS = sSall + (size_t)e * 2 * G * 64;
     int t = 0;
@@ -271,11 +286,10 @@ __global__ void __launch_bounds__(32 * (kTcEGWarps + 2 + NSW), 1)
       ++t;
     }
     if (lane == 0 && sy.trace) STEP_TRACE(2 + warp);
-  } else {
+  } else if (warp >= kTcSamplerWarp0) {
     // ---------------- sampler group ----------------
-    // 4 samples in flight per half-warp: this kernel serves large batches (many rounds per item
-    // anyway) and must fit 448 threads x 128 registers without spilling
-    step_sampler_loop<T, D, G, NSW, 4>(sp, sy, samp_smem, tag32, tag8);
+    setmaxnreg_inc<200>();
+    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag8);
   }
   // ---------------- teardown: TMEM, then the exit ticket (the last CTA out advances the epoch) ----
   tc_fence_before();
