@@ -175,25 +175,58 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   const int nC = (seqlen + p.L - 1) / p.L;
 
   // ---- a3: chunk stats -> fp64 chunk CDF ------------------------------------------------------
+  // thread t owns the contiguous chunks [t*per, t*per + per); for <= 8 per thread (nC <= 8 NT) they
+  // are loaded straight into registers (one round trip), W_c = 2^(m_c - m*) l_c with the power in fp32
+  // (ex2.approx, 2 ulp -- the fp32 scores already carry errors of that order) and the sums, the CDF
+  // and the in-chunk rescale in fp64 (as the step kernel, reading #24)
   const float2* cs = p.cstats + bh * p.Cmax;
-  float mloc = -INFINITY;
-  for (int c = tid; c < nC; c += NT) {
-    const float2 v = __ldcg(cs + c);
-    sC[c] = v;
-    mloc = fmaxf(mloc, v.x);
-  }
-  const float mstar = block_max_f(mloc, sred_f);  // (its barrier also publishes sC)
-  SANTA_TRACE(3);
   const int per = (nC + NT - 1) / NT;
-  const int c0 = tid * per, c1 = min(c0 + per, nC);
+  const int c0 = min(tid * per, nC), c1 = min(c0 + per, nC);
+  constexpr int kCPT = 8;
   double part = 0.0;
   int lastpos = -1;
-  for (int c = c0; c < c1; ++c) {
-    const float2 st = sC[c];
-    const double w = st.y > 0.f ? exp2((double)st.x - (double)mstar) * (double)st.y : 0.0;
-    sF[c] = w;
-    part += w;
-    if (w > 0.0) lastpos = c;
+  if (per <= kCPT) {
+    float2 st[kCPT];
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i) st[i] = (c0 + i < c1) ? __ldcg(cs + c0 + i) : make_float2(-INFINITY, 0.f);
+    float mloc = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i) mloc = fmaxf(mloc, st[i].x);
+    const float mstar = block_max_f(mloc, sred_f);
+    SANTA_TRACE(3);
+#pragma unroll
+    for (int i = 0; i < kCPT; ++i) {
+      if (c0 + i >= c1) break;
+      const float w32 = st[i].y > 0.f ? ex2(st[i].x - mstar) : 0.f;  // 2^(m_c - m*)
+      const double w = (double)w32 * (double)st[i].y;
+      sF[c0 + i] = w;
+      // in-chunk rescale Z 2^(m* - m_c) = Z l_c / W_c: store 1 / 2^(m_c - m*) now, times Z below
+      reinterpret_cast<double*>(sC)[c0 + i] = w > 0.0 ? 1.0 / (double)w32 : 0.0;
+      part += w;
+      if (w > 0.0) lastpos = c0 + i;
+    }
+  } else {  // long sequences in 64-key chunks: the smem loop
+    float mloc = -INFINITY;
+    for (int c = tid; c < nC; c += NT) {
+      const float2 v = __ldcg(cs + c);
+      sC[c] = v;
+      mloc = fmaxf(mloc, v.x);
+    }
+    const float mstar = block_max_f(mloc, sred_f);  // (its barrier also publishes sC)
+    SANTA_TRACE(3);
+    for (int c = c0; c < c1; ++c) {
+      const float2 st = sC[c];
+      const float w32 = st.y > 0.f ? ex2(st.x - mstar) : 0.f;
+      const double w = (double)w32 * (double)st.y;
+      sF[c] = w;
+      part += w;
+      if (w > 0.0) lastpos = c;
+    }
+    __syncthreads();  // every thread has read its sC entries before they are overwritten
+    for (int c = c0; c < c1; ++c) {
+      const double w = sF[c];
+      reinterpret_cast<double*>(sC)[c] = w > 0.0 ? (double)sC[c].y / w : 0.0;  // l_c / W_c
+    }
   }
   double Z;
   double run = block_excl_scan_d(part, sred_d, &Z);
@@ -203,8 +236,7 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
     const double w = sF[c];
     run += w;
     sF[c] = c >= lastpos ? 1.0 : run * invZ;
-    // in-chunk rescale Z * 2^(m* - m_c) = Z l_c / W_c, kept in the chunk's (now unused) slot
-    reinterpret_cast<double*>(sC)[c] = w > 0.0 ? Z * (double)sC[c].y / w : 0.0;
+    reinterpret_cast<double*>(sC)[c] *= Z;  // Z l_c / W_c
   }
   SANTA_TRACE(4);
   // ---- sequence sharding: this rank's slice of the global shard CDF --------------------------
