@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
 }
 
 template <typename T, int D, int G>
-__global__ void __launch_bounds__(kScoreThreads, 4) bern_chunk_kernel(BernParams p) {
+__global__ void __launch_bounds__(kScoreThreads, (sizeof(T) == 2 && G <= 4) ? 8 : 4) bern_chunk_kernel(BernParams p) {
   __shared__ __align__(16) float sS[G * kDenseChunk];
   __shared__ __align__(16) float sAcc[4][G][kDenseChunk];
   __shared__ float sW[G][D];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kScoreThreads, 4) bern_chunk_kernel(BernParams
   const bool live = kl < n_valid;
   // UF selected feature rows per warp in flight (16-B loads issued before any is consumed): one load
   // per lane per feature leaves ~6 KiB in flight per SM, far below what HBM needs (measured 0.37 of peak)
-  constexpr int UF = sizeof(T) == 2 ? 8 : 4;
+  constexpr int UF = (sizeof(T) == 2 && G <= 4) ? 4 : (sizeof(T) == 2 ? 8 : 4);  // rows in flight per warp
   for (int s0 = warp; s0 < nsel; s0 += 4 * UF) {
     uint4 r[UF][sizeof(T) == 2 ? 1 : 2];
 #pragma unroll
