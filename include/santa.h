@@ -109,12 +109,14 @@ const char* santa_version(void);
  * the seq-shard phases / santa_bernoulli_scores for this geometry and budget S
  * (pure host arithmetic; returns 0 if the geometry is invalid).  The same workspace
  * may be reused across calls on one stream (one call at a time); it must be 256-byte
- * aligned and ZERO-INITIALISED ONCE before its first use: the single-launch step kernel
- * keeps its cross-CTA synchronisation counters in it, zero at rest, and every counter is
- * reset by its last user inside each launch (so no per-call memset is needed).  A
- * workspace whose counters are not zero makes the step kernel time out (~0.5 s) and
- * raise SANTA_FLAG_SYNC_TIMEOUT instead of hanging.  Everything else in it is
- * initialised by the kernels. */
+ * aligned and ZERO-INITIALISED ONCE before its first use: the single-launch step kernels
+ * keep a launch epoch and split/exit tickets in it (tickets are zero at rest -- each is
+ * reset by its last user inside the launch -- and the epoch advances once per launch), and
+ * publish their cross-CTA data as words tagged with the epoch, so stale words of earlier
+ * launches are never taken for current ones and no per-call memset is needed.  On a
+ * workspace that was not zeroed a stale word could carry the current tag (~2^-32 per word)
+ * or a poll could wait for its ~0.5 s timeout (SANTA_FLAG_SYNC_TIMEOUT) -- never a hang.
+ * Everything else in it is initialised by the kernels. */
 size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
 
 /* SANTA / S^2ANTA decode step (the north-star hot path; Eq. 4):
@@ -131,9 +133,11 @@ size_t santa_workspace_bytes(const santa_geometry* geo, int32_t S);
  * 128-multiple pages, the whole step is ONE cooperative persistent launch (the tcgen05 step kernel:
  * interleaved TMA score stream, score stage on tensor cores with TMEM accumulators, each
  * (b, kv-head) unit sampled as soon as its chunks are scored, chunk results published as tagged
- * words -- no fences); otherwise the split-KV score pass + a PDL-chained sampler kernel.  The two paths draw the same thresholds and chunk CDFs; their
- * in-chunk prefixes are fp32 (two-kernel) vs 24-bit fixed point (step kernel, DESIGN.md reading
- * #23), so an index may differ only where a threshold lies within ~2^-24 of a key boundary. */
+ * words -- no fences); otherwise the split-KV score pass + a PDL-chained sampler kernel.
+ * All paths draw the same thresholds; their chunk CDFs agree up to fp32/fp64 summation order and
+ * their in-chunk prefixes are fp32 (two-kernel) vs 24-bit fixed point (step kernels, DESIGN.md
+ * reading #23), so an index may differ between paths only where a threshold lies within ~2^-24
+ * of a key boundary (the oracle-parity exemption of reading #19 covers it). */
 santa_status santa_decode_attention(const santa_geometry* geo, const void* q, const void* K,
                                     const void* V, const int32_t* seqlens, int32_t S,
                                     int32_t mode, uint64_t seed, uint64_t offset, void* out,
@@ -156,17 +160,19 @@ santa_status santa_decode_attention_profiled(const santa_geometry* geo, const vo
  * (a santa_path value; -1 if the geometry is invalid).  Pure host logic. */
 int32_t santa_auto_path(const santa_geometry* geo, int32_t S);
 
-/* santa_decode_attention with an explicit execution path (santa_path); AUTO is exactly
- * santa_decode_attention.  Used by the tests and bench.py to compare the two paths. */
+/* santa_decode_attention with an explicit execution path (santa_path: AUTO, STEP_KERNEL,
+ * TWO_KERNEL, STEP_TC); AUTO is exactly santa_decode_attention.  A forced path that does not
+ * support the geometry (e.g. a step kernel on an fp32 cache) returns SANTA_ERR_UNSUPPORTED and
+ * launches nothing.  Used by the tests and bench.py to compare the paths. */
 santa_status santa_decode_attention_path(const santa_geometry* geo, const void* q, const void* K,
                                          const void* V, const int32_t* seqlens, int32_t S,
                                          int32_t mode, uint64_t seed, uint64_t offset, void* out,
                                          int32_t* idx_out, void* workspace,
                                          size_t workspace_bytes, int32_t path, void* stream);
 
-/* The two phases of santa_decode_attention, exposed separately (same arguments and
+/* The two phases of the two-kernel path, exposed separately (same arguments and
  * workspace; calling santa_score_phase then santa_sample_phase on one stream is exactly
- * santa_decode_attention).  Phase 1 = the split-KV score pass:
+ * santa_decode_attention_path(..., SANTA_PATH_TWO_KERNEL, ...)).  Phase 1 = the split-KV score pass:
  * it reads every K byte and leaves the per-chunk (m_c, l_c) and the fp32 prefix stash in
  * `workspace`.  Phase 2 = combine + thresholds + inverse CDF + gather-add (rows a3-a6). */
 santa_status santa_score_phase(const santa_geometry* geo, const void* q, const void* K,
