@@ -391,6 +391,17 @@ struct RunSample {
 // The whole step in one pipelined cooperative launch (step_kernel.cuh).  Returns
 // SANTA_ERR_UNSUPPORTED (nothing launched) when the configuration does not qualify, in which
 // case the caller runs the two-kernel path.
+// A cooperative launch the device cannot co-schedule (e.g. SMs held by another context) is
+// "unsupported here", not a failure: AUTO then runs the two-kernel path.
+santa_status coop_status(cudaError_t e) {
+  if (e == cudaSuccess) return SANTA_OK;
+  if (e == cudaErrorCooperativeLaunchTooLarge) {
+    cudaGetLastError();  // clear the sticky-free launch error
+    return SANTA_ERR_UNSUPPORTED;
+  }
+  return SANTA_ERR_CUDA;
+}
+
 StepSync make_step_sync(const DecodeArgs& a) {
   StepSync sy;
   uint32_t* base = at<uint32_t>(a.ws, a.L.sync);
@@ -443,8 +454,7 @@ struct RunStep {
       attr[0].val.cooperative = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, kern, tk, tq, sp, pq, sy) != cudaSuccess) return SANTA_ERR_CUDA;
-      return SANTA_OK;
+      return coop_status(cudaLaunchKernelEx(&cfg, kern, tk, tq, sp, pq, sy));
     }
   }
 
@@ -496,8 +506,7 @@ struct RunStep {
       attr[0].val.cooperative = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      if (cudaLaunchKernelEx(&cfg, kern, tm, sp, pp, sy) != cudaSuccess) return SANTA_ERR_CUDA;
-      return SANTA_OK;
+      return coop_status(cudaLaunchKernelEx(&cfg, kern, tm, sp, pp, sy));
     }
   }
 };
