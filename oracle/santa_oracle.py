@@ -569,3 +569,122 @@ def fidelity(approx, exact) -> tuple[float, float]:
     if ne == 0:
         raise ValueError("undefined relative error")
     return float(np.linalg.norm(a - e) / ne), float(a @ e / (np.linalg.norm(a) * ne))
+
+
+# ---------------------------------------------------------------------------
+# 9. S^2ANTA-prop with largest-remainder tile budgets (
+#    App. M, Alg. prop-pass1, Alg. prop-budgets P:1597-1613,
+#    Alg. prop-pass2; mini version P:1556-1573)
+# ---------------------------------------------------------------------------
+
+TAG_PROP_TILE_OFFSET = 4   # reading #25: tag 4 -> a_{0,h,t}, draw index = tile t
+
+
+def prop_tile_stats(s: np.ndarray, B_tile: int):
+    """Kernel 1 (P:1585-1591): T = ceil(n_k / B_tile) tiles T_t = [t B_tile, min((t+1) B_tile, n_k));
+    m_t = max_{n in T_t} s_n, l_t = sum_{n in T_t} exp(s_n - m_t), u_n = exp(s_n - m_t) (the optional
+    u-stash).  Returns (m [T], l [T], u [n_k]) in fp64."""
+    s = np.asarray(s, dtype=np.float64)
+    n = s.shape[0]
+    if n < 1 or B_tile < 1:
+        raise ValueError("empty distribution")
+    T = -(-n // B_tile)
+    m = np.empty(T)
+    l = np.empty(T)
+    u = np.empty(n)
+    for t in range(T):
+        lo, hi = t * B_tile, min((t + 1) * B_tile, n)
+        m[t] = s[lo:hi].max()
+        u[lo:hi] = np.exp(s[lo:hi] - m[t])
+        l[t] = u[lo:hi].sum()
+    return m, l, u
+
+
+def largest_remainder(q: np.ndarray, S: int) -> np.ndarray:
+    """S_t = floor(q_t), then the remaining S - sum_t S_t samples one each to the tiles with the
+    largest fractional part of q_t; equal fractional parts go to the lower tile
+    index (S:282, reading #25).  q: quotas [T] fp64 summing to S."""
+    q = np.asarray(q, dtype=np.float64)
+    fl = np.floor(q)
+    St = fl.astype(np.int64)
+    R = S - int(St.sum())
+    if R < 0 or R > q.shape[0]:
+        raise ValueError("quotas do not sum to S")
+    frac = q - fl
+    order = sorted(range(q.shape[0]), key=lambda t: (-frac[t], t))
+    for t in order[:R]:
+        St[t] += 1
+    return St
+
+
+def prop_budgets(m: np.ndarray, l: np.ndarray, S: int):
+    """Kernel 2 for one head: m* = max_t m_t, W_t = exp(m_t - m*) l_t, Z = sum_t W_t,
+    q_t = S W_t / Z, S_t = largest_remainder(q, S), invdelta_t = S_t / l_t if S_t > 0 else 0.
+    Returns (S_t [T] int64, invdelta [T], q [T])."""
+    m = np.asarray(m, dtype=np.float64)
+    l = np.asarray(l, dtype=np.float64)
+    mstar = m.max()
+    W = np.exp(m - mstar) * l
+    Z = W.sum()
+    q = S * W / Z
+    St = largest_remainder(q, S)
+    invd = np.where(St > 0, St / np.where(l > 0, l, 1.0), 0.0)
+    return St, invd, q
+
+
+def prop_counts(u: np.ndarray, B_tile: int, invdelta: np.ndarray, a0: np.ndarray) -> np.ndarray:
+    """Kernel 3 counts, literally: per tile, p = 0; for n increasing:
+    x = invdelta_t u_n; c_n = floor(a0_t + p + x) - floor(a0_t + p); p += x."""
+    n = u.shape[0]
+    c = np.zeros(n, dtype=np.int64)
+    for t in range(invdelta.shape[0]):
+        p = 0.0
+        for i in range(t * B_tile, min((t + 1) * B_tile, n)):
+            x = invdelta[t] * u[i]
+            c[i] = int(math.floor(a0[t] + p + x) - math.floor(a0[t] + p))
+            p += x
+    return c
+
+
+def santa_prop_decode(q, K, V, seqlens, S: int, seed: int, offset: int = 0, B_tile: int = 64,
+                      scale: Optional[float] = None, batch_offset: int = 0, head_offset: int = 0,
+                      return_details: bool = False):
+    """The S^2ANTA-prop decode step (Alg. prop-mini) for every (b, h), kv = floor(h/G):
+    scores over j < seqlens[b] -> Kernel 1 tile stats -> Kernel 2 budgets (a0_t = Philox tag 4,
+    draw t, reading #25) -> Kernel 3 counts -> O = sum_n c_n V_n, out = O / S.
+    idx [B, H, S]: the emitted rows, tile-major, each row repeated c_n times (the GPU's order).
+    Returns out [B, H, d] fp64, idx (and details {(b,h): (St, q, a0, c)} if requested)."""
+    qf = to_f64(q)
+    B, H, d = qf.shape
+    G = H // K.shape[1]
+    scale = 1.0 / math.sqrt(d) if not scale else scale
+    out = np.zeros((B, H, d))
+    idx = np.zeros((B, H, S), dtype=np.int64)
+    det = {}
+    for b in range(B):
+        n = int(seqlens[b])
+        if n < 1:
+            raise ValueError("empty distribution")
+        for h in range(H):
+            kv = h // G
+            Kb = _seq_kv(K, b, kv, n)
+            Vb = _seq_kv(V, b, kv, n)
+            s = scores(qf[b, h], Kb, scale)
+            m, l, u = prop_tile_stats(s, B_tile)
+            St, invd, qt = prop_budgets(m, l, S)
+            a0 = philox_uniforms(seed, offset, TAG_PROP_TILE_OFFSET, head_offset + h, batch_offset + b,
+                                 np.arange(m.shape[0]))
+            c = prop_counts(u, B_tile, invd, a0)
+            J = np.repeat(np.arange(n), c)
+            if J.shape[0] != S:
+                raise ValueError("emitted sample count differs from S")
+            acc = np.zeros(d)
+            for i in np.nonzero(c)[0]:
+                acc += c[i] * Vb[i]
+            out[b, h] = acc / S
+            idx[b, h] = J
+            if return_details:
+                det[(b, h)] = {"St": St, "q": qt, "a0": a0, "c": c, "m": m, "l": l, "u": u}
+    if return_details:
+        return out, idx, det
+    return out, idx
