@@ -559,6 +559,34 @@ def main():
                                 "achieved_GBps": round(sach, 1), "frac": round(sach / peak, 4)}
         paths["sample_phase_us"] = round(sgms * 1e3, 2)
         res["paths"] = paths
+        # (1c) S^2ANTA-prop (the paper's own estimator): score pass + budget/count/gather
+        # kernel, at this S and at the paper's prop operating point S = 128
+        prop = {"estimator": "S^2ANTA-prop, largest-remainder tile budgets, B_tile = 64 (App. M)"}
+        for Sp in sorted({args.S, 128}):
+            pws = santa.workspace(p0.geo, Sp, dev)
+            pidx = torch.empty((B, H, Sp), dtype=torch.int32, device=dev)
+            pu = []
+            for i in range(4):
+                santa.santa_decode_attention_prop(p0.geo, p0.q, p0.K, p0.V, p0.seqlens, Sp, args.seed, i, p0.out,
+                                                  pidx, pws, stream)
+                torch.cuda.synchronize()
+                ii = pidx.cpu().numpy()
+                pu.append(sum(len(np.unique(ii[b, g * G:(g + 1) * G])) for b in range(B) for g in range(Hkv)))
+            pkb, pvb, pqo = algorithmic_bytes([n] * B, Hkv, d, 2, float(np.mean(pu)), B, H)
+
+            def propp(i, Sp=Sp, pws=pws):
+                p = probs[i % NR]
+                santa.santa_decode_attention_prop(p.geo, p.q, p.K, p.V, p.seqlens, Sp, args.seed, i, p.out, None,
+                                                  pws, stream)
+            for i in range(args.warmup):
+                propp(i)
+            t = max_over_ranks(timed_loop(propp, args.steps))
+            prop[f"S{Sp}"] = {"us_per_step": round(t * 1e3, 2),
+                              "GBps": round((pkb + pvb + pqo) / (t * 1e-3) / 1e9, 1),
+                              "frac": round((pkb + pvb + pqo) / (t * 1e-3) / 1e9 / peak, 4),
+                              "unique_rows": float(np.mean(pu)), "launches_per_step": 2}
+            del pws
+        res["prop"] = prop
         # (2) isolated single-step latency, the paper's protocol (flush write before each step)
         iso = []
         for i in range(args.steps):

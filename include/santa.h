@@ -183,6 +183,29 @@ santa_status santa_sample_phase(const santa_geometry* geo, const void* V, const 
                                 int32_t* idx_out, void* workspace, size_t workspace_bytes,
                                 void* stream);
 
+/* S^2ANTA-prop decode step (App. M, Algs. prop-pass1 P:1577-1594,
+ * prop-budgets P:1597-1613, prop-pass2 P:1616-1641): the paper's proportional-allocation
+ * estimator, a DIFFERENT (slightly biased) estimator from santa_decode_attention's global
+ * samplers.  Per (b, h): tile stats m_t, l_t over tiles of B_tile = santa_prop_tile_len(geo) keys
+ * (the score pass's chunks), W_t = exp(m_t - m*) l_t, quotas q_t = S W_t / Z, integer budgets
+ * S_t = floor(q_t) plus one each to the S - sum floor(q_t) tiles of largest fractional part (ties
+ * to the lower tile; fractional parts compared to 2^-40), then per tile systematic counts
+ * c_n = floor(a0_t + p + x) - floor(a0_t + p), x = (S_t / l_t) exp(s_n - m_t), with
+ * a0_t = Philox(seed, offset, tag 4, head_offset + h, batch_offset + b) draw t (reading #25);
+ * out = (1/S) sum_n c_n V_n.  idx_out (optional) [B, H, S]: the emitted rows, tile-major, each
+ * repeated c_n times.  Arguments, layouts, workspace and errors as santa_decode_attention (no
+ * mode: the per-tile rule is systematic).  Two launches: the score pass, then the budget +
+ * count + gather kernel (PDL-chained). */
+santa_status santa_decode_attention_prop(const santa_geometry* geo, const void* q, const void* K,
+                                         const void* V, const int32_t* seqlens, int32_t S,
+                                         uint64_t seed, uint64_t offset, void* out,
+                                         int32_t* idx_out, void* workspace,
+                                         size_t workspace_bytes, void* stream);
+
+/* The tile length B_tile santa_decode_attention_prop uses for this geometry (64 up to 512k
+ * tokens; -1 if the geometry is invalid).  Pure host logic. */
+int32_t santa_prop_tile_len(const santa_geometry* geo);
+
 /* Exact dense decode attention softmax(q K^T * scale) V (Eq. 1) with the same
  * split-KV score pass and a flash-decoding LSE combine; the in-repo reference the SANTA
  * latency is reported against.  Arguments as above. */

@@ -59,6 +59,8 @@ def _load() -> ctypes.CDLL:
         "santa_decode_attention_path": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, i32, vp], i32),
         "santa_decode_attention_profiled": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp, vp], i32),
         "santa_dense_reference": ([G, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+        "santa_decode_attention_prop": ([G, vp, vp, vp, vp, i32, u64, u64, vp, vp, vp, sz, vp], i32),
+        "santa_prop_tile_len": ([G], i32),
         "santa_score_phase": ([G, vp, vp, vp, vp, sz, vp], i32),
         "santa_sample_phase": ([G, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_bernoulli_scores": ([G, vp, vp, vp, i32, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),

@@ -125,6 +125,142 @@ __host__ __device__ inline size_t sample_smem_bytes(int Cmax, int S_local, int D
   return (size_t)Cmax * 16 + (size_t)S_local * 16 + (size_t)(nthreads / 16 + 1) * D * 4 + 64;
 }
 
+// a5 (part 2) + a6 for the Sl samples of one work item whose chunk sChunk[m] (-1: not sampled
+// here) and in-chunk threshold sTl[m] are in shared memory: a HALF-WARP per sample finds
+// k = min{k : P_c[k] > sTl[m]} in the chunk's prefix block (ballots, L = 64; binary search
+// otherwise), writes idx_out[bh, m_lo + m], then loads and adds the V row; the half-warps'
+// sums are reduced in fixed order into sPart [D] (unscaled).  All threads call it.
+template <typename T, int D>
+__device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
+                                                  int Sl, int m_lo, int seqlen, const int* sChunk,
+                                                  const float* sTl, float* sRed, float* sPart) {
+  const int NT = blockDim.x, NHW = NT >> 4;
+  const int tid = threadIdx.x;
+  const int S = p.S;
+  constexpr int EB = (int)sizeof(T);
+  constexpr int VCH = D * EB / 16;                  // 16-B chunks per V row
+  constexpr int NCH = (VCH + 15) / 16;              // chunks per lane
+  constexpr int EPC = 16 / EB;                      // elements per chunk
+  constexpr int U = 8;                              // samples in flight per half-warp
+  const int hw = tid >> 4, l = tid & 15;
+  const unsigned hmask = 0xffffu << (threadIdx.x & 16);
+  float acc[NCH][EPC];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q)
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
+  const T* Vb = reinterpret_cast<const T*>(p.V);
+  const float* Pbase = p.stash + bh * p.stash_stride;
+  // V row address: contiguous caches hoist the (b, kv-head) base (one multiply-add per row; the
+  // generic paged/contiguous KvLayout::row() inlined per sample serialised the loads' issue)
+  const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
+  auto vrow = [&](int t) -> const T* {
+    return p.kv.page_table ? Vb + p.kv.row(b, kvh, t, D) : vbase + (int64_t)t * D;
+  };
+  const int tok0 = p.token_offset ? __ldg(p.token_offset + b) : 0;
+  // warp-uniform trip count: warp w walks sample pairs 2w, 2w+1 (+ NHW per u); the full-mask
+  // ballots below must be reached by both half-warps
+  for (int mw = 2 * (tid >> 5); mw < Sl; mw += NHW * U) {
+    const int m0 = mw + (hw & 1);
+    int jj[U];
+    float4 pv[U];
+    int cc[U], nn[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NHW;
+      cc[u] = m < Sl ? sChunk[m] : -1;
+      nn[u] = cc[u] >= 0 ? min(p.L, seqlen - cc[u] * p.L) : 0;
+      pv[u] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      if (cc[u] >= 0 && p.L == 64 && 4 * l < nn[u])
+        pv[u] = ldcg_f4(reinterpret_cast<const float4*>(Pbase + (size_t)cc[u] * p.L) + l);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      // in-chunk index k = min{k : P[k] > tf} = #{k : P[k] <= tf} (P non-decreasing; inactive samples
+      // and keys beyond the sequence load P = +inf).  L = 64, branch-free: one ballot over every
+      // lane's last value (lane j holds keys 4j..4j+3) + the crossing lane's own count.
+      const int m = m0 + u * NHW;
+      const bool on = cc[u] >= 0;
+      const float tf = on ? sTl[m] : -INFINITY;
+      const float4 v = pv[u];
+      int k;
+      if (p.L == 64) {
+        const int full_lanes = __popc(__ballot_sync(0xffffffffu, v.w <= tf) & hmask);
+        const int own = (v.x <= tf) + (v.y <= tf) + (v.z <= tf) + (v.w <= tf);
+        const int cross = __shfl_sync(0xffffffffu, own, (tid & 16) + min(full_lanes, 15));
+        k = full_lanes < 16 ? 4 * full_lanes + cross : 64;
+        // rounding put tf at/after the chunk's total: the first key reaching the total (the last
+        // positive-mass key); the total P[n-1] sits in lane (n-1)/4, component (n-1)%4
+        if (__any_sync(0xffffffffu, on && k >= nn[u])) {
+          const int ln = max(nn[u] - 1, 0);
+          const int src = (tid & 16) + (ln >> 2);
+          const float tx = __shfl_sync(0xffffffffu, v.x, src), ty = __shfl_sync(0xffffffffu, v.y, src);
+          const float tz = __shfl_sync(0xffffffffu, v.z, src), tw = __shfl_sync(0xffffffffu, v.w, src);
+          const float tot = (ln & 3) == 0 ? tx : (ln & 3) == 1 ? ty : (ln & 3) == 2 ? tz : tw;
+          const int fl2 = __popc(__ballot_sync(0xffffffffu, v.w < tot) & hmask);
+          const int own2 = (v.x < tot) + (v.y < tot) + (v.z < tot) + (v.w < tot);
+          const int cross2 = __shfl_sync(0xffffffffu, own2, (tid & 16) + min(fl2, 15));
+          if (on && k >= nn[u]) k = fl2 < 16 ? 4 * fl2 + cross2 : nn[u] - 1;
+        }
+      } else {
+        k = 0;
+        if (on) {
+          const float* P = Pbase + (size_t)cc[u] * p.L;
+          k = thread_chunk_search(P, nn[u], tf);
+          if (k >= nn[u]) k = thread_chunk_search(P, nn[u], nextafterf(__ldcg(P + nn[u] - 1), -INFINITY));
+        }
+      }
+      jj[u] = on ? cc[u] * p.L + min(k, nn[u] - 1) : -1;
+      if (on && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u] + tok0;
+      if (!on && m < Sl && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = -1;  // another shard's stratum
+    }
+    if (mw == 0) SANTA_TRACE(8);  // indices known (stash loaded, ballots done)
+    uint4 raw[U][NCH];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        const int ch = l + 16 * q;
+        raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(vrow(jj[u]) + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        if constexpr (EB == 2) {
+          const uint32_t w[4] = {raw[u][q].x, raw[u][q].y, raw[u][q].z, raw[u][q].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[q][2 * e] += Elem<T>::lo(w[e]);
+            acc[q][2 * e + 1] += Elem<T>::hi(w[e]);
+          }
+        } else {
+          acc[q][0] += __uint_as_float(raw[u][q].x);
+          acc[q][1] += __uint_as_float(raw[u][q].y);
+          acc[q][2] += __uint_as_float(raw[u][q].z);
+          acc[q][3] += __uint_as_float(raw[u][q].w);
+        }
+      }
+  }
+  SANTA_TRACE(9);  // V rows gathered and added (thread 0)
+  // deterministic reduction over the half-warps (fixed order)
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const int ch = l + 16 * q;
+    if (ch < VCH)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) sRed[hw * D + ch * EPC + e] = acc[q][e];
+  }
+  __syncthreads();
+  SANTA_TRACE(6);
+  for (int d = tid; d < D; d += NT) {
+    float s = 0.f;
+    for (int r = 0; r < NHW; ++r) s += sRed[r * D + d];
+    sPart[d] = s;
+  }
+  __syncthreads();
+}
+
 // One (b, h, split) work item.  Leaves the CTA's partial sum sum_{own m} V_{J_m} (fp32, not yet
 // scaled by 1/S) in the returned shared array [D]; the caller reduces/scales/writes it.  All
 // threads of the block must call it.  Empty sequences (seqlen < 1) give a zero partial, idx -1
@@ -301,129 +437,8 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   __syncthreads();
   SANTA_TRACE(5);
 
-  // ---- a5 (part 2) + a6: half-warp per sample: in-chunk search + gather-add ---------------------
-  constexpr int EB = (int)sizeof(T);
-  constexpr int VCH = D * EB / 16;                  // 16-B chunks per V row
-  constexpr int NCH = (VCH + 15) / 16;              // chunks per lane
-  constexpr int EPC = 16 / EB;                      // elements per chunk
-  constexpr int U = 8;                              // samples in flight per half-warp
-  const int hw = tid >> 4, l = tid & 15;
-  const unsigned hmask = 0xffffu << (threadIdx.x & 16);
-  float acc[NCH][EPC];
-#pragma unroll
-  for (int q = 0; q < NCH; ++q)
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
-  const T* Vb = reinterpret_cast<const T*>(p.V);
-  const float* Pbase = p.stash + bh * p.stash_stride;
-  // V row address: contiguous caches hoist the (b, kv-head) base (one multiply-add per row; the
-  // generic paged/contiguous KvLayout::row() inlined per sample serialised the loads' issue)
-  const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
-  auto vrow = [&](int t) -> const T* {
-    return p.kv.page_table ? Vb + p.kv.row(b, kvh, t, D) : vbase + (int64_t)t * D;
-  };
-  const int tok0 = p.token_offset ? __ldg(p.token_offset + b) : 0;
-  // warp-uniform trip count: warp w walks sample pairs 2w, 2w+1 (+ NHW per u); the full-mask
-  // ballots below must be reached by both half-warps
-  for (int mw = 2 * (tid >> 5); mw < Sl; mw += NHW * U) {
-    const int m0 = mw + (hw & 1);
-    int jj[U];
-    float4 pv[U];
-    int cc[U], nn[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int m = m0 + u * NHW;
-      cc[u] = m < Sl ? sChunk[m] : -1;
-      nn[u] = cc[u] >= 0 ? min(p.L, seqlen - cc[u] * p.L) : 0;
-      pv[u] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-      if (cc[u] >= 0 && p.L == 64 && 4 * l < nn[u])
-        pv[u] = ldcg_f4(reinterpret_cast<const float4*>(Pbase + (size_t)cc[u] * p.L) + l);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      // in-chunk index k = min{k : P[k] > tf} = #{k : P[k] <= tf} (P non-decreasing; inactive samples
-      // and keys beyond the sequence load P = +inf).  L = 64, branch-free: one ballot over every
-      // lane's last value (lane j holds keys 4j..4j+3) + the crossing lane's own count.
-      const int m = m0 + u * NHW;
-      const bool on = cc[u] >= 0;
-      const float tf = on ? sTl[m] : -INFINITY;
-      const float4 v = pv[u];
-      int k;
-      if (p.L == 64) {
-        const int full_lanes = __popc(__ballot_sync(0xffffffffu, v.w <= tf) & hmask);
-        const int own = (v.x <= tf) + (v.y <= tf) + (v.z <= tf) + (v.w <= tf);
-        const int cross = __shfl_sync(0xffffffffu, own, (tid & 16) + min(full_lanes, 15));
-        k = full_lanes < 16 ? 4 * full_lanes + cross : 64;
-        // rounding put tf at/after the chunk's total: the first key reaching the total (the last
-        // positive-mass key); the total P[n-1] sits in lane (n-1)/4, component (n-1)%4
-        if (__any_sync(0xffffffffu, on && k >= nn[u])) {
-          const int ln = max(nn[u] - 1, 0);
-          const int src = (tid & 16) + (ln >> 2);
-          const float tx = __shfl_sync(0xffffffffu, v.x, src), ty = __shfl_sync(0xffffffffu, v.y, src);
-          const float tz = __shfl_sync(0xffffffffu, v.z, src), tw = __shfl_sync(0xffffffffu, v.w, src);
-          const float tot = (ln & 3) == 0 ? tx : (ln & 3) == 1 ? ty : (ln & 3) == 2 ? tz : tw;
-          const int fl2 = __popc(__ballot_sync(0xffffffffu, v.w < tot) & hmask);
-          const int own2 = (v.x < tot) + (v.y < tot) + (v.z < tot) + (v.w < tot);
-          const int cross2 = __shfl_sync(0xffffffffu, own2, (tid & 16) + min(fl2, 15));
-          if (on && k >= nn[u]) k = fl2 < 16 ? 4 * fl2 + cross2 : nn[u] - 1;
-        }
-      } else {
-        k = 0;
-        if (on) {
-          const float* P = Pbase + (size_t)cc[u] * p.L;
-          k = thread_chunk_search(P, nn[u], tf);
-          if (k >= nn[u]) k = thread_chunk_search(P, nn[u], nextafterf(__ldcg(P + nn[u] - 1), -INFINITY));
-        }
-      }
-      jj[u] = on ? cc[u] * p.L + min(k, nn[u] - 1) : -1;
-      if (on && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = jj[u] + tok0;
-      if (!on && m < Sl && l == 0 && p.idx_out) p.idx_out[bh * S + m_lo + m] = -1;  // another shard's stratum
-    }
-    if (mw == 0) SANTA_TRACE(8);  // indices known (stash loaded, ballots done)
-    uint4 raw[U][NCH];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int q = 0; q < NCH; ++q) {
-        const int ch = l + 16 * q;
-        raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(vrow(jj[u]) + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
-      }
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-      for (int q = 0; q < NCH; ++q) {
-        if constexpr (EB == 2) {
-          const uint32_t w[4] = {raw[u][q].x, raw[u][q].y, raw[u][q].z, raw[u][q].w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            acc[q][2 * e] += Elem<T>::lo(w[e]);
-            acc[q][2 * e + 1] += Elem<T>::hi(w[e]);
-          }
-        } else {
-          acc[q][0] += __uint_as_float(raw[u][q].x);
-          acc[q][1] += __uint_as_float(raw[u][q].y);
-          acc[q][2] += __uint_as_float(raw[u][q].z);
-          acc[q][3] += __uint_as_float(raw[u][q].w);
-        }
-      }
-  }
-  SANTA_TRACE(9);  // V rows gathered and added (thread 0)
-  // deterministic reduction over the half-warps (fixed order)
-#pragma unroll
-  for (int q = 0; q < NCH; ++q) {
-    const int ch = l + 16 * q;
-    if (ch < VCH)
-#pragma unroll
-      for (int e = 0; e < EPC; ++e) sRed[hw * D + ch * EPC + e] = acc[q][e];
-  }
-  __syncthreads();
-  SANTA_TRACE(6);
-  for (int d = tid; d < D; d += NT) {
-    float s = 0.f;
-    for (int r = 0; r < NHW; ++r) s += sRed[r * D + d];
-    sPart[d] = s;
-  }
-  __syncthreads();
+  // ---- a5 (part 2) + a6 ---------------------------------------------------------------------------
+  gather_chunk_rows<T, D>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart);
   return sPart;
 }
 
@@ -433,17 +448,13 @@ __device__ __forceinline__ void store_out(const SampleParams& p, size_t bh, int 
   else reinterpret_cast<T*>(p.out)[bh * D + d] = Elem<T>::from_f(v);
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(SampleParams p) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+// Sum the partials of the CS CTAs of one head's cluster (through DSMEM, fixed rank order), scale
+// by 1/S and store the head's output.
+template <typename T, int D>
+__device__ __forceinline__ void finish_head(const SampleParams& p, size_t bh, int rank, int CS, float* sPart) {
   namespace cg = cooperative_groups;
-  const int CS = p.cluster;
-  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const int h = blockIdx.x / CS, b = blockIdx.y;
-  const size_t bh = (size_t)b * p.H + h;
-  float* sPart = sample_item<T, D, G>(p, b, h, rank, CS, smem_raw);
   const float invS = 1.0f / (float)p.S;
-  if (CS > 1) {  // sum the cluster's partials through DSMEM in fixed rank order
+  if (CS > 1) {
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
     if (rank == 0)
@@ -456,6 +467,18 @@ __global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(Sample
   } else {
     for (int d = threadIdx.x; d < D; d += blockDim.x) store_out<T, D>(p, bh, d, sPart[d] * invS);
   }
+}
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(SampleParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  namespace cg = cooperative_groups;
+  const int CS = p.cluster;
+  const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const int h = blockIdx.x / CS, b = blockIdx.y;
+  const size_t bh = (size_t)b * p.H + h;
+  float* sPart = sample_item<T, D, G>(p, b, h, rank, CS, smem_raw);
+  finish_head<T, D>(p, bh, rank, CS, sPart);
   if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[bh * 16 + 7] = gtimer();
 }
 

@@ -11,6 +11,7 @@
 #include "dense_kernels.cuh"
 #include "dense_stream_kernel.cuh"
 #include "philox.cuh"
+#include "prop_kernels.cuh"
 #include "sample_kernels.cuh"
 #include "score_kernels.cuh"
 #include "step_kernel.cuh"
@@ -384,6 +385,44 @@ struct RunSample {
     cfg.numAttrs = na;
     if (cudaLaunchKernelEx(&cfg, sample_gather_kernel<T, D, G>, p) != cudaSuccess) return SANTA_ERR_CUDA;
     if (a.events) cudaEventRecord(a.events[2], a.st);
+    return SANTA_OK;
+  }
+};
+
+// S^2ANTA-prop budgets + counts + gather (prop_kernels.cuh), PDL-chained to the score pass; the
+// same cluster split of the S samples as RunSample.
+template <typename T, int D, int G>
+struct RunProp {
+  static santa_status run(const DecodeArgs& a) {
+    SampleParams p = make_sample_params(a);
+    int CS = 1;
+    const int heads = a.g->batch * a.g->n_heads;
+    while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
+    p.cluster = CS;
+    const size_t smem = prop_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
+    if (smem > 227 * 1024) return SANTA_ERR_UNSUPPORTED;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      if (cudaFuncSetAttribute(prop_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      configured = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
+    cfg.blockDim = dim3(kSampleThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, prop_gather_kernel<T, D, G>, p) != cudaSuccess) return SANTA_ERR_CUDA;
     return SANTA_OK;
   }
 };
@@ -844,6 +883,31 @@ santa_status santa_sample_phase(const santa_geometry* g, const void* V, const in
   const int G = g->n_heads / g->n_kv_heads;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   return last_cuda();
+}
+
+santa_status santa_decode_attention_prop(const santa_geometry* g, const void* q, const void* K, const void* V,
+                                         const int32_t* seqlens, int32_t S, uint64_t seed, uint64_t offset,
+                                         void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
+  if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
+  if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 3u)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = SANTA_SYSTEMATIC;
+  a.seed = seed; a.offset = offset; a.out = out; a.idx_out = idx_out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  if ((s = dispatch<RunProp>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+int32_t santa_prop_tile_len(const santa_geometry* g) {
+  if (validate_geometry(g) != SANTA_OK) return -1;
+  return layout(g, 1).L;
 }
 
 santa_status santa_dense_reference(const santa_geometry* g, const void* q, const void* K, const void* V,

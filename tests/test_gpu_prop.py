@@ -1,0 +1,209 @@
+"""S^2ANTA-prop on the GPU vs the oracle's santa_prop_decode, through the C ABI
+(-m gpu).  The budgets S_t are integer decisions taken from floating point: the oracle takes them
+from fp64 scores, the kernel from the score pass's fp32 tile stats, so a head whose budgets differ
+is accepted only if the GPU's budgets are a valid largest-remainder allocation of the ORACLE's
+quotas within a tolerance (reading #25); heads with equal budgets must agree row by row except
+where the oracle's count boundary a0 + invdelta U_n lies within a tolerance of the integer j."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import santa_inputs as si  # noqa: E402
+from oracle import santa_oracle as o  # noqa: E402
+
+try:
+    import paper_2605_01910_b200 as santa  # noqa: E402
+    from gpu_helpers import TOL, to_cuda  # noqa: E402
+except ImportError:  # library not built: the gpu tests must fail loudly, not skip
+    santa = None
+
+
+@pytest.fixture(autouse=True)
+def _need_lib():
+    assert santa is not None, "libsanta.so not built"
+    assert torch.cuda.is_available(), "no CUDA device"
+
+
+def gpu_prop(inp, S, seed, offset=0, paged=False, head_offset=0, batch_offset=0, max_seqlen=None):
+    if paged:
+        out, idx = santa.decode_prop(inp.q, inp.K_pool, inp.V_pool, inp.seqlens, S, seed, offset,
+                                     n_kv_heads=inp.n_kv_heads, page_table=inp.page_table,
+                                     page_size=inp.page_size, max_seqlen=max_seqlen or inp.max_seqlen,
+                                     return_idx=True, head_offset=head_offset, batch_offset=batch_offset)
+    else:
+        out, idx = santa.decode_prop(inp.q, inp.K, inp.V, inp.seqlens, S, seed, offset, max_seqlen=max_seqlen,
+                                     return_idx=True, head_offset=head_offset, batch_offset=batch_offset)
+    torch.cuda.synchronize()
+    return out, idx
+
+
+def lr_valid(Sg, q, S, tol):
+    """Sg is a largest-remainder allocation of quotas within tol of q: sum = S, every S_t within
+    1 + tol of q_t, and no tile rounded down keeps a larger remainder than a tile rounded up."""
+    if int(Sg.sum()) != S or np.any(np.abs(Sg - q) >= 1 + tol):
+        return False
+    up = Sg > q
+    down_rem = (q - Sg)[~up]
+    up_rem = (1.0 - (Sg - q))[up]
+    if down_rem.size == 0 or up_rem.size == 0:
+        return True
+    return down_rem.max() <= up_rem.min() + 2 * tol
+
+
+def prop_parity(inp, out_g, idx_g, S, seed, offset=0, head_offset=0, batch_offset=0, B_tile=64,
+                max_budget_mismatch=0.25):
+    """Returns (heads, heads with different budgets, samples compared, index mismatches, exempt)."""
+    q, K, V = si.as_bits(inp.q), si.as_bits(inp.K), si.as_bits(inp.V)
+    seqlens = inp.seqlens.cpu().numpy()
+    _, idx_o, det = o.santa_prop_decode(q, K, V, seqlens, S, seed, offset, B_tile=B_tile,
+                                        head_offset=head_offset, batch_offset=batch_offset, return_details=True)
+    idx_g = idx_g.cpu().numpy().astype(np.int64)
+    tol_q = 2e-5 * S + 1e-9
+    heads = budget_diff = compared = mism = exempt = 0
+    for (b, h), dd in det.items():
+        heads += 1
+        n = int(seqlens[b])
+        ig = idx_g[b, h]
+        assert ig.min() >= 0 and ig.max() < n and np.all(np.diff(ig) >= 0), (b, h)
+        T = dd["St"].shape[0]
+        Sg = np.bincount(ig // B_tile, minlength=T)
+        assert Sg.shape[0] == T
+        if not np.array_equal(Sg, dd["St"]):
+            budget_diff += 1
+            assert lr_valid(Sg, dd["q"], S, tol_q), (b, h, np.nonzero(Sg != dd["St"]))
+            continue
+        # equal budgets: the same tile-major sample list up to count boundaries at rounding distance
+        io = idx_o[b, h]
+        u, a0, St = dd["u"], dd["a0"], dd["St"]
+        for m in np.nonzero(io != ig)[0]:
+            t = io[m] // B_tile
+            j = m - int(St[:t].sum()) + 1
+            lo, hi = min(io[m], ig[m]), max(io[m], ig[m])
+            Ut = np.cumsum(u[t * B_tile:min((t + 1) * B_tile, n)]) * (St[t] / dd["l"][t])
+            y = a0[t] + Ut[lo - t * B_tile:hi - t * B_tile]
+            tol_c = 1e-5 * St[t] + 1e-6
+            assert np.all(np.abs(y - j) <= tol_c), (b, h, m, io[m], ig[m], y - j)
+            exempt += 1
+        mism += int((io != ig).sum())
+        compared += S
+    assert budget_diff <= max_budget_mismatch * heads, (budget_diff, heads)
+    ref = o.out_given_idx(V, idx_g)
+    got = out_g.float().cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max()
+    assert err <= TOL[inp.dtype], f"output max-abs err {err} > {TOL[inp.dtype]}"
+    return heads, budget_diff, compared, mism, exempt
+
+
+def test_tile_len_is_the_chunk_length():
+    q = torch.zeros(1, 8, 128, dtype=torch.bfloat16)
+    assert santa.santa_prop_tile_len(santa.make_geometry(q, 2, 32768)) == 64
+    assert santa.santa_prop_tile_len(santa.make_geometry(q, 2, 1 << 20)) == 128
+
+
+@pytest.mark.parametrize("paged", [False, True])
+def test_prop_bf16_gqa_ragged(paged):
+    """Llama GQA shape (H=32, H_kv=8, d=128, bf16), ragged seqlens with partial last tiles,
+    contiguous and shuffled paged (P=64) caches."""
+    inp = to_cuda(si.make_decode_inputs(2, 32, 8, 128, [4097, 1000], dtype="bf16", seed=2,
+                                        page_size=64 if paged else 0))
+    out, idx = gpu_prop(inp, 256, seed=11, offset=3, paged=paged)
+    r = prop_parity(inp, out, idx, 256, 11, 3)
+    print("prop gqa", paged, r)
+
+
+@pytest.mark.parametrize("dtype,d,H,Hkv", [("f16", 64, 16, 2), ("bf16", 64, 8, 8), ("f32", 128, 16, 8),
+                                            ("bf16", 128, 4, 2)])
+def test_prop_dtype_shape_variants(dtype, d, H, Hkv):
+    inp = to_cuda(si.make_decode_inputs(2, H, Hkv, d, [777, 2048], dtype=dtype, seed=3, workload="temp4"))
+    out, idx = gpu_prop(inp, 64, seed=5)
+    prop_parity(inp, out, idx, 64, 5)
+
+
+@pytest.mark.parametrize("workload", ["temp4", "sink"])
+def test_prop_peaked_workloads(workload):
+    """Peaked profiles: most tiles get budget 0, a few get many samples."""
+    inp = to_cuda(si.make_decode_inputs(1, 32, 8, 128, 3000, dtype="bf16", seed=4, workload=workload))
+    out, idx = gpu_prop(inp, 128, seed=9)
+    prop_parity(inp, out, idx, 128, 9)
+
+
+def test_prop_edge_cases():
+    """seqlen 1 (one tile of one key), S = 1, S > n_k, S = 4096 (the budget limit), and a cache
+    padded to a much larger max_seqlen (same result)."""
+    inp = to_cuda(si.make_decode_inputs(3, 8, 2, 128, [1, 17, 300], dtype="bf16", seed=5))
+    for S in (1, 3, 100, 1024, 4096):
+        out, idx = gpu_prop(inp, S, seed=S)
+        prop_parity(inp, out, idx, S, S)
+        assert torch.all(idx[0] == 0)
+    out1, idx1 = gpu_prop(inp, 64, seed=1)
+    pad = torch.nn.functional.pad
+    big = si.DecodeInputs(q=inp.q, K=pad(inp.K, (0, 0, 0, 4700)).contiguous(),
+                          V=pad(inp.V, (0, 0, 0, 4700)).contiguous(), seqlens=inp.seqlens, n_heads=8,
+                          n_kv_heads=2, head_dim=128, dtype="bf16")
+    out2, idx2 = gpu_prop(big, 64, seed=1)
+    assert torch.equal(idx1, idx2) and torch.equal(out1, out2)
+
+
+def test_prop_empty_sequence_sets_flag():
+    inp = to_cuda(si.make_decode_inputs(2, 8, 2, 128, [5, 40], dtype="bf16", seed=6))
+    inp.seqlens[0] = 0
+    geo = santa.make_geometry(inp.q, 2, 40)
+    ws = santa.workspace(geo, 8)
+    out = torch.full_like(inp.q, 7.0)
+    idx = torch.empty((2, 8, 8), dtype=torch.int32, device="cuda")
+    santa.santa_decode_attention_prop(geo, inp.q, inp.K, inp.V, inp.seqlens, 8, 1, 0, out, idx, ws)
+    assert santa.santa_read_error_flags(ws) & santa.FLAG_EMPTY_SEQ
+    assert torch.all(out[0] == 0) and torch.all(idx[0] == -1)
+    assert torch.all(idx[1] >= 0) and torch.all(idx[1] < 40)
+
+
+def test_prop_determinism_and_stream_keys():
+    """Bitwise reproducible; seed, offset, head_offset and batch_offset each change the a0 stream."""
+    inp = to_cuda(si.make_decode_inputs(2, 8, 2, 128, [3000, 2000], dtype="bf16", seed=8))
+    out1, idx1 = gpu_prop(inp, 128, seed=3, offset=1)
+    out2, idx2 = gpu_prop(inp, 128, seed=3, offset=1)
+    assert torch.equal(idx1, idx2) and torch.equal(out1, out2)
+    for kw in (dict(seed=4, offset=1), dict(seed=3, offset=2), dict(seed=3, offset=1, head_offset=8),
+               dict(seed=3, offset=1, batch_offset=2)):
+        _, idx3 = gpu_prop(inp, 128, **kw)
+        assert not torch.equal(idx1, idx3)
+    out4, idx4 = gpu_prop(inp, 128, seed=3, offset=1, head_offset=8, batch_offset=2)
+    prop_parity(inp, out4, idx4, 128, 3, 1, head_offset=8, batch_offset=2)
+
+
+def test_prop_full_size_config2_sampled_heads():
+    """BASELINE config-2 size (32k tokens, batch 1, H=32, H_kv=8, S=256) in the launch configuration
+    bench.py times; the oracle recomputes two kv-head groups (8 heads)."""
+    inp = to_cuda(si.make_decode_inputs(1, 32, 8, 128, 32768, dtype="bf16", seed=0))
+    out, idx = gpu_prop(inp, 256, seed=0x5A17A)
+    for kvh in (0, 5):
+        sub = si.DecodeInputs(q=inp.q[:, 4 * kvh:4 * kvh + 4].contiguous(), K=inp.K[:, kvh:kvh + 1].contiguous(),
+                              V=inp.V[:, kvh:kvh + 1].contiguous(), seqlens=inp.seqlens, n_heads=4, n_kv_heads=1,
+                              head_dim=128, dtype="bf16")
+        r = prop_parity(sub, out[:, 4 * kvh:4 * kvh + 4], idx[:, 4 * kvh:4 * kvh + 4], 256, 0x5A17A,
+                        head_offset=4 * kvh)
+        print("prop c2-full", kvh, r)
+
+
+def test_prop_unbiased_on_integer_quotas_gpu():
+    """Tiles holding permutations of the same keys give integer quotas; the GPU estimate averaged over
+    seeds then converges to dense attention (the oracle's exact-expectation pin, on the kernel)."""
+    B_tile, T, d = 64, 8, 128
+    g = torch.Generator().manual_seed(3)
+    base_k = torch.randn(B_tile, d, generator=g)
+    perm = [torch.randperm(B_tile, generator=g) for _ in range(T)]
+    K = torch.cat([base_k[p] for p in perm])[None, None].to(torch.bfloat16)
+    V = torch.randn(1, 1, B_tile * T, d, generator=g).to(torch.bfloat16)
+    q = (torch.randn(1, 1, d, generator=g) * 0.5).to(torch.bfloat16)
+    seqlens = torch.tensor([B_tile * T], dtype=torch.int32)
+    Kc, Vc, qc, sc = K.cuda(), V.cuda(), q.cuda(), seqlens.cuda()
+    S, N = 16, 2000
+    acc = torch.zeros(d, dtype=torch.float64, device="cuda")
+    for seed in range(N):
+        acc += santa.decode_prop(qc, Kc, Vc, sc, S, seed=seed)[0, 0].double()
+    mean = (acc / N).cpu().numpy()
+    exact = o.dense_decode(si.as_bits(q), si.as_bits(K), si.as_bits(V), [B_tile * T])[0, 0]
+    # per-seed spread is bounded by max|V|; N seeds; within-tile systematic sampling
+    assert np.abs(mean - exact).max() < 6 * float(V.float().abs().max()) / np.sqrt(N * S)
