@@ -11,9 +11,10 @@
 // boundary after the score pass, which this kernel waits on with griddepcontrol (PDL).
 //   budgets  m* = max_t m_t, W_t = 2^(m_t - m*) l_t (fp64), Z = sum W_t (fixed-order block scan),
 //            q_t = S W_t / Z, S_t = floor(q_t) + one each to the R = S - sum floor(q_t) tiles of
-//            largest fractional part, ties to the lower tile index: a bitonic sort of the
-//            keys (frac quantised to 2^-40 | inverted tile index) in shared memory; the top R keys
-//            carry their tile index.  Exclusive scan of S_t -> tile offsets.
+//            largest fractional part, ties to the lower tile index: the R largest keys
+//            (frac quantised to 2^-40 | inverted tile index) by an MSB radix select in shared
+//            memory, finished by an exact in-warp rank of the <= 32 boundary keys (a bitonic sort
+//            measured 45% of the kernel).  Exclusive scan of S_t -> tile offsets.
 //   counts   Alg. prop-pass2's c_n = floor(a0 + p + x) - floor(a0 + p), p = invdelta U_{n-1}, is
 //            the number of integers j in (a0 + invdelta U_{n-1}, a0 + invdelta U_n]; so the j-th
 //            sample of tile t (j = 1..S_t) is row min{n : U_n >= (j - a0_t) l_t / S_t} (reading #25),
@@ -26,14 +27,8 @@
 
 namespace santa {
 
-__host__ __device__ inline int prop_tpad(int Cmax) {
-  int t = 1;
-  while (t < Cmax) t <<= 1;
-  return t;
-}
-
 __host__ __device__ inline size_t prop_smem_bytes(int Cmax, int S_local, int D, int nthreads) {
-  return (size_t)prop_tpad(Cmax) * 8 + (size_t)Cmax * 8 + (size_t)(Cmax + 1) * 4 + (size_t)S_local * 8 +
+  return (size_t)Cmax * 8 + (size_t)Cmax * 8 + (size_t)(Cmax + 1) * 4 + (size_t)S_local * 8 +
          (size_t)(nthreads / 16 + 1) * D * 4 + 64;
 }
 
@@ -47,9 +42,8 @@ __device__ float* prop_item(const SampleParams& p, int b, int h, int rank, int C
   const int m_lo = (int)((long long)S * rank / CS), m_hi = (int)((long long)S * (rank + 1) / CS);
   const int Sl = m_hi - m_lo;
   const int Slmax = (S + CS - 1) / CS;
-  const int Tpad_max = prop_tpad(p.Cmax);
-  unsigned long long* sKey = reinterpret_cast<unsigned long long*>(smem_raw);  // [Tpad]
-  float2* sCs = reinterpret_cast<float2*>(sKey + Tpad_max);                    // [Cmax] tile stats
+  unsigned long long* sKey = reinterpret_cast<unsigned long long*>(smem_raw);  // [Cmax] LR keys
+  float2* sCs = reinterpret_cast<float2*>(sKey + p.Cmax);                      // [Cmax] tile stats
   int* sOff = reinterpret_cast<int*>(sCs + p.Cmax);                            // [Cmax + 1]
   int* sChunk = sOff + p.Cmax + 1;                                             // [Slmax]
   float* sTl = reinterpret_cast<float*>(sChunk + Slmax);                       // [Slmax]
@@ -57,6 +51,8 @@ __device__ float* prop_item(const SampleParams& p, int b, int h, int rank, int C
   float* sPart = sRed + NHW * D;                                               // [D]
   __shared__ double sred_d[32];
   __shared__ float sred_f[32];
+  __shared__ int sHist[256], sSel[3], sNcand, sFlag[32];
+  __shared__ unsigned long long sCand[32];
 
   pdl_wait_primary();
   const int seqlen = __ldg(p.seqlens + b);
@@ -69,8 +65,6 @@ __device__ float* prop_item(const SampleParams& p, int b, int h, int rank, int C
     return sPart;
   }
   const int nC = (seqlen + p.L - 1) / p.L;
-  int Tpad = 1;
-  while (Tpad < nC) Tpad <<= 1;
 
   // ---- Kernel 2: m*, W_t, Z -----------------------------------------------------------------
   const float2* cs = p.cstats + bh * p.Cmax;
@@ -104,28 +98,85 @@ __device__ float* prop_item(const SampleParams& p, int b, int h, int rank, int C
     sKey[c] = ((unsigned long long)(frac * 1099511627776.0) << 23) | (unsigned long long)(0x7FFFFF - c);
     flsum += fl;
   }
-  for (int c = nC + tid; c < Tpad; c += NT) sKey[c] = 0ull;  // padding sorts last
   double flt;
   (void)block_excl_scan_d(flsum, sred_d, &flt);  // (barrier: keys and floors visible)
   const int R = min(max(S - (int)flt, 0), nC);
 
-  if (R > 0) {  // bitonic sort of the keys, descending
-    for (int k = 2; k <= Tpad; k <<= 1)
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = tid; i < Tpad; i += NT) {
-          const int ixj = i ^ j;
-          if (ixj > i) {
-            const unsigned long long x = sKey[i], y = sKey[ixj];
-            const bool desc = (i & k) == 0;
-            if (desc ? (x < y) : (x > y)) {
-              sKey[i] = y;
-              sKey[ixj] = x;
-            }
-          }
-        }
-        __syncthreads();
+  if (R > 0) {
+    // the R largest keys by MSB radix select (8-bit digits, 63-bit keys): each pass histograms the
+    // digit of the keys that match the selected prefix so far and fixes the digit at which the
+    // running count from the top reaches `need`; as soon as the boundary bin holds <= 32 keys they
+    // are ranked exactly inside one warp.  Keys are unique (tile index in the low bits).
+    unsigned long long prefix = 0ull, pmask = 0ull;
+    int need = R;
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = tid; i < 256; i += NT) sHist[i] = 0;
+      if (tid == 0) sNcand = 0;
+      __syncthreads();
+      for (int c = c0; c < c1; ++c) {
+        const unsigned long long k = sKey[c];
+        if ((k & pmask) == prefix) atomicAdd(&sHist[(int)((k >> shift) & 255ull)], 1);
       }
-    for (int r = tid; r < R; r += NT) sOff[0x7FFFFF - (int)(sKey[r] & 0x7FFFFFull)] += 1;
+      __syncthreads();
+      if (tid < 32) {  // warp 0: digit d with above(d) < need <= above(d) + hist[d], from the top
+        int cnt[8], run = 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          cnt[e] = sHist[255 - (tid * 8 + e)];  // lane 0 holds the largest digits
+          run += cnt[e];
+        }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += v;
+        }
+        int above = incl - run;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          if (above < need && need <= above + cnt[e]) {
+            sSel[0] = 255 - (tid * 8 + e);
+            sSel[1] = above;
+            sSel[2] = cnt[e];
+          }
+          above += cnt[e];
+        }
+      }
+      __syncthreads();
+      const int d = sSel[0];
+      need -= sSel[1];
+      prefix |= (unsigned long long)d << shift;
+      pmask |= 255ull << shift;
+      if (sSel[2] == need || sSel[2] <= 32 || shift == 0) break;
+      __syncthreads();  // sSel / sHist are rewritten by the next pass
+    }
+    // selected: keys above the prefix; of those equal to it, all (bin exactly filled) or the `need`
+    // largest, ranked in one warp
+    const bool all_bin = sSel[2] == need;
+    if (!all_bin) {
+      for (int c = c0; c < c1; ++c)
+        if ((sKey[c] & pmask) == prefix) sCand[atomicAdd(&sNcand, 1)] = sKey[c];
+      __syncthreads();
+      if (tid < 32) {
+        const int nc = sNcand;  // <= 32 (or, at shift 0, unique full keys: <= 1)
+        const unsigned long long mine = tid < nc ? sCand[tid] : 0ull;
+        int rank = 0;
+        for (int i = 0; i < nc; ++i) rank += sCand[i] > mine;
+        sFlag[tid] = (tid < nc && rank < need) ? 1 : 0;
+      }
+      __syncthreads();
+    }
+    for (int c = c0; c < c1; ++c) {
+      const unsigned long long k = sKey[c];
+      bool sel = (k & pmask) > prefix;
+      if ((k & pmask) == prefix) {
+        if (all_bin) sel = true;
+        else
+          for (int i = 0; i < sNcand; ++i)
+            if (sCand[i] == k) sel = sFlag[i] != 0;
+      }
+      if (sel) sOff[c] += 1;
+    }
     __syncthreads();
   }
 

@@ -207,3 +207,22 @@ def test_prop_unbiased_on_integer_quotas_gpu():
     exact = o.dense_decode(si.as_bits(q), si.as_bits(K), si.as_bits(V), [B_tile * T])[0, 0]
     # per-seed spread is bounded by max|V|; N seeds; within-tile systematic sampling
     assert np.abs(mean - exact).max() < 6 * float(V.float().abs().max()) / np.sqrt(N * S)
+
+
+@pytest.mark.parametrize("T,S", [(40, 60), (40, 100), (100, 150), (300, 1000)])
+def test_prop_exact_ties_go_to_lower_tiles(T, S):
+    """Every tile holds the same 64 keys and values, so all quotas q_t = S/T are bit-identical on both
+    sides and the largest-remainder extras must go to the lowest tile indices -- with 100 or
+    300 tied keys the radix select runs down to the tile-index digits."""
+    g = torch.Generator().manual_seed(T + S)
+    K = torch.randn(1, 1, 64, 128, generator=g).repeat(1, 1, T, 1).to(torch.bfloat16)
+    V = torch.randn(1, 1, 64, 128, generator=g).repeat(1, 1, T, 1).to(torch.bfloat16)
+    q = torch.randn(1, 2, 128, generator=g).to(torch.bfloat16)
+    inp = to_cuda(si.DecodeInputs(q=q, K=K, V=V, seqlens=torch.tensor([64 * T], dtype=torch.int32), n_heads=2,
+                                  n_kv_heads=1, head_dim=128, dtype="bf16"))
+    out, idx = gpu_prop(inp, S, seed=7)
+    base, R = divmod(S, T)
+    want = np.array([base + 1] * R + [base] * (T - R))
+    for h in range(2):
+        assert np.array_equal(np.bincount(idx[0, h].cpu().numpy() // 64, minlength=T), want)
+    prop_parity(inp, out, idx, S, 7, max_budget_mismatch=0.0)
