@@ -688,3 +688,73 @@ def santa_prop_decode(q, K, V, seqlens, S: int, seed: int, offset: int = 0, B_ti
     if return_details:
         return out, idx, det
     return out, idx
+
+
+# ---------------------------------------------------------------------------
+# 10. S^2ANTA-flash: uniform per-tile budgets + deferred LSE merge (
+#     App. N: overview P:1651-1667, Kernel 1 P:1669-1689, Kernel 2 P:1691-1706)
+# ---------------------------------------------------------------------------
+
+TAG_FLASH_TILE_OFFSET = 5  # reading #26: tag 5 -> flash a_{0,h,t}, draw index = tile t
+
+
+def flash_tile_budget(n: int, B_tile: int, S: int) -> int:
+    """S_tile ~ S / T 'rounded', T = ceil(n_k / B_tile): round half up, at least 1
+    (reading #26 -- a tile with budget 0 would drop its mass from the estimator)."""
+    T = -(-n // B_tile)
+    return max(1, int(math.floor(S / T + 0.5)))
+
+
+def flash_merge(m: np.ndarray, l: np.ndarray, O_tilde: np.ndarray, S_tile: int) -> np.ndarray:
+    """Kernel 2: m* = max_t m_t, W_t = exp(m_t - m*) l_t, Z = sum_t W_t,
+    O = (1/Z) sum_t W_t (O~_t / S_tile)."""
+    m = np.asarray(m, dtype=np.float64)
+    l = np.asarray(l, dtype=np.float64)
+    W = np.exp(m - m.max()) * l
+    Z = W.sum()
+    return (W[:, None] * (np.asarray(O_tilde, dtype=np.float64) / S_tile)).sum(0) / Z
+
+
+def santa_flash_decode(q, K, V, seqlens, S: int, seed: int, offset: int = 0, B_tile: int = 256,
+                       scale: Optional[float] = None, batch_offset: int = 0, head_offset: int = 0,
+                       return_details: bool = False):
+    """The S^2ANTA-flash decode step for every (b, h), kv = floor(h/G): Kernel 1 per tile
+    m_t, u_n = exp(s_n - m_t), l_t, invdelta_t = S_tile / l_t, a0_t = Philox tag 5 draw t, systematic
+    counts c_n (the same loop as prop-pass2), O~_t = sum_{n in T_t} c_n V_n; Kernel 2
+    flash_merge.  idx [B, H, M_max]: the rows drawn (tile-major, each c_n times; M_b = S_tile(b) T_b,
+    padded with -1).  Returns out [B, H, d] fp64, idx (and details if requested)."""
+    qf = to_f64(q)
+    B, H, d = qf.shape
+    G = H // K.shape[1]
+    scale = 1.0 / math.sqrt(d) if not scale else scale
+    Mmax = max(flash_tile_budget(int(n), B_tile, S) * -(-int(n) // B_tile) for n in seqlens)
+    out = np.zeros((B, H, d))
+    idx = np.full((B, H, Mmax), -1, dtype=np.int64)
+    det = {}
+    for b in range(B):
+        n = int(seqlens[b])
+        if n < 1:
+            raise ValueError("empty distribution")
+        S_tile = flash_tile_budget(n, B_tile, S)
+        for h in range(H):
+            kv = h // G
+            Kb = _seq_kv(K, b, kv, n)
+            Vb = _seq_kv(V, b, kv, n)
+            s = scores(qf[b, h], Kb, scale)
+            m, l, u = prop_tile_stats(s, B_tile)
+            T = m.shape[0]
+            invd = S_tile / l
+            a0 = philox_uniforms(seed, offset, TAG_FLASH_TILE_OFFSET, head_offset + h, batch_offset + b,
+                                 np.arange(T))
+            c = prop_counts(u, B_tile, invd, a0)
+            O_t = np.zeros((T, d))
+            for i in np.nonzero(c)[0]:
+                O_t[i // B_tile] += c[i] * Vb[i]
+            out[b, h] = flash_merge(m, l, O_t, S_tile)
+            J = np.repeat(np.arange(n), c)
+            idx[b, h, :J.shape[0]] = J
+            if return_details:
+                det[(b, h)] = {"S_tile": S_tile, "a0": a0, "c": c, "m": m, "l": l, "u": u}
+    if return_details:
+        return out, idx, det
+    return out, idx
