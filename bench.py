@@ -587,6 +587,33 @@ def main():
                               "unique_rows": float(np.mean(pu)), "launches_per_step": 2}
             del pws
         res["prop"] = prop
+        # (1d) S^2ANTA-flash at the paper's operating point (tile 256, S = 2048)
+        # and at this S: score pass + per-tile draw / merge-weighted gather kernel
+        flash = {"estimator": "S^2ANTA-flash, uniform per-tile budgets + LSE merge (App. N)"}
+        for Sf, tile in ((2048, 256), (args.S, 256)):
+            fws = santa.workspace(p0.geo, Sf, dev)
+            Mf = santa.santa_flash_max_samples(p0.geo, Sf, tile)
+            fidx = torch.empty((B, H, Mf), dtype=torch.int32, device=dev)
+            santa.santa_decode_attention_flash(p0.geo, p0.q, p0.K, p0.V, p0.seqlens, Sf, tile, args.seed, 0,
+                                               p0.out, fidx, fws, stream)
+            torch.cuda.synchronize()
+            ii = fidx.cpu().numpy()
+            fu = sum(len(np.unique(ii[b, g * G:(g + 1) * G])) for b in range(B) for g in range(Hkv))
+            fkb, fvb, fqo = algorithmic_bytes([n] * B, Hkv, d, 2, float(fu), B, H)
+
+            def flashp(i, Sf=Sf, tile=tile, fws=fws):
+                p = probs[i % NR]
+                santa.santa_decode_attention_flash(p.geo, p.q, p.K, p.V, p.seqlens, Sf, tile, args.seed, i, p.out,
+                                                   None, fws, stream)
+            for i in range(args.warmup):
+                flashp(i)
+            t = max_over_ranks(timed_loop(flashp, args.steps))
+            flash[f"S{Sf}_tile{tile}"] = {"us_per_step": round(t * 1e3, 2),
+                                          "GBps": round((fkb + fvb + fqo) / (t * 1e-3) / 1e9, 1),
+                                          "frac": round((fkb + fvb + fqo) / (t * 1e-3) / 1e9 / peak, 4),
+                                          "rows_per_head": Mf, "unique_rows": fu, "launches_per_step": 2}
+            del fws
+        res["flash"] = flash
         # (2) isolated single-step latency, the paper's protocol (flush write before each step)
         iso = []
         for i in range(args.steps):

@@ -206,6 +206,30 @@ santa_status santa_decode_attention_prop(const santa_geometry* geo, const void* 
  * tokens; -1 if the geometry is invalid).  Pure host logic. */
 int32_t santa_prop_tile_len(const santa_geometry* geo);
 
+/* S^2ANTA-flash decode step (App. N, Algs. flash-mini P:1651-1667, flash-k1
+ * P:1669-1689, flash-k2 P:1691-1706): uniform per-tile budgets and a deferred LSE merge -- an
+ * exactly unbiased estimator that draws samples in every tile ("sample waste").  Per (b, h):
+ * T = ceil(n / tile_len) tiles, S_tile = max(1, floor(S / T + 1/2)) (reading #26); in every tile
+ * the systematic rows of u_n = exp(s_n - m_t) with invdelta = S_tile / l_t and
+ * a0_t = Philox(seed, offset, tag 5, head_offset + h, batch_offset + b) draw t; then
+ * out = (1/Z) sum_t W_t O~_t / S_tile, W_t = exp(m_t - m*) l_t, Z = sum_t W_t, O~_t = sum of the
+ * tile's rows.  tile_len: a positive multiple of santa_prop_tile_len(geo) (the score pass's chunk),
+ * at most 64 chunks (the paper's operating point: 256 with S = 2048 at 32k tokens);
+ * otherwise SANTA_ERR_INVALID_ARG.  idx_out (optional) [B, H, M] int32 with
+ * M = santa_flash_max_samples(geo, S, tile_len): the rows drawn, tile-major, -1 past the head's
+ * S_tile * T; M > 16384 returns SANTA_ERR_UNSUPPORTED.  Other arguments, layouts, workspace and
+ * errors as santa_decode_attention (no mode).  Two launches: the score pass, then the per-tile
+ * draw + merge-weighted gather kernel (PDL-chained; the merge is folded into the gather). */
+santa_status santa_decode_attention_flash(const santa_geometry* geo, const void* q, const void* K,
+                                          const void* V, const int32_t* seqlens, int32_t S,
+                                          int32_t tile_len, uint64_t seed, uint64_t offset, void* out,
+                                          int32_t* idx_out, void* workspace, size_t workspace_bytes,
+                                          void* stream);
+
+/* Row length M of santa_decode_attention_flash's idx_out: the largest S_tile * T over sequence
+ * lengths <= geo->max_seqlen (-1 if the geometry, S or tile_len is invalid).  Pure host logic. */
+int32_t santa_flash_max_samples(const santa_geometry* geo, int32_t S, int32_t tile_len);
+
 /* Exact dense decode attention softmax(q K^T * scale) V (Eq. 1) with the same
  * split-KV score pass and a flash-decoding LSE combine; the in-repo reference the SANTA
  * latency is reported against.  Arguments as above. */

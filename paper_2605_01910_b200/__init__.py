@@ -22,7 +22,8 @@ __all__ = [
     "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes", "santa_auto_path",
     "santa_decode_attention", "santa_decode_attention_path", "santa_decode_attention_profiled", "santa_score_phase",
     "santa_sample_phase", "PATHS", "FLAG_SYNC_TIMEOUT",
-    "santa_dense_reference", "santa_decode_attention_prop", "santa_prop_tile_len",
+    "santa_dense_reference", "santa_decode_attention_prop", "santa_prop_tile_len", "santa_decode_attention_flash",
+    "santa_flash_max_samples", "decode_flash",
     "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
     "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_decode_step_host_packed", "santa_philox_uniforms",
     "santa_read_error_flags", "santa_version", "decode", "decode_prop", "dense", "LIB_PATH",
@@ -135,6 +136,21 @@ def santa_prop_tile_len(geo: Geometry) -> int:
     return n
 
 
+def santa_decode_attention_flash(geo, q, K, V, seqlens, S, tile_len, seed, offset, out, idx_out, ws, stream=None):
+    """S^2ANTA-flash (uniform per-tile budgets + LSE merge; include/santa.h)."""
+    _abi.check("santa_decode_attention_flash", _abi.LIB.santa_decode_attention_flash(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, tile_len, seed, offset, _ptr(out),
+        _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def santa_flash_max_samples(geo: Geometry, S: int, tile_len: int) -> int:
+    """idx_out row length of santa_decode_attention_flash (pure host logic)."""
+    n = int(_abi.LIB.santa_flash_max_samples(ctypes.byref(geo), S, tile_len))
+    if n < 1:
+        raise SantaError("santa_flash_max_samples", 1)
+    return n
+
+
 def santa_dense_reference(geo, q, K, V, seqlens, out, ws, stream=None):
     _abi.check("santa_dense_reference", _abi.LIB.santa_dense_reference(
         ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), _ptr(out), _ptr(ws), ws.numel(),
@@ -235,6 +251,23 @@ def decode_prop(q, K, V, seqlens, S, seed=0, offset=0, n_kv_heads=None, page_tab
     out = torch.empty_like(q)
     idx = torch.empty((q.shape[0], q.shape[1], S), dtype=torch.int32, device=q.device) if return_idx else None
     santa_decode_attention_prop(geo, q, K, V, seqlens, S, seed, offset, out, idx, ws)
+    return (out, idx) if return_idx else out
+
+
+def decode_flash(q, K, V, seqlens, S, tile_len=256, seed=0, offset=0, n_kv_heads=None, page_table=None,
+                 page_size=0, max_seqlen=None, return_idx=False, ws=None, batch_offset=0, head_offset=0):
+    """Allocate out (+ idx [B, H, santa_flash_max_samples]) and workspace, run santa_decode_attention_flash."""
+    Hkv = n_kv_heads or K.shape[1]
+    n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    geo = make_geometry(q, Hkv, n_max, page_table, page_size, batch_offset=batch_offset, head_offset=head_offset)
+    if ws is None:
+        ws = workspace(geo, S, q.device)
+    out = torch.empty_like(q)
+    idx = None
+    if return_idx:
+        M = santa_flash_max_samples(geo, S, tile_len)
+        idx = torch.empty((q.shape[0], q.shape[1], M), dtype=torch.int32, device=q.device)
+    santa_decode_attention_flash(geo, q, K, V, seqlens, S, tile_len, seed, offset, out, idx, ws)
     return (out, idx) if return_idx else out
 
 

@@ -61,6 +61,8 @@ def _load() -> ctypes.CDLL:
         "santa_dense_reference": ([G, vp, vp, vp, vp, vp, vp, sz, vp], i32),
         "santa_decode_attention_prop": ([G, vp, vp, vp, vp, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_prop_tile_len": ([G], i32),
+        "santa_decode_attention_flash": ([G, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
+        "santa_flash_max_samples": ([G, i32, i32], i32),
         "santa_score_phase": ([G, vp, vp, vp, vp, sz, vp], i32),
         "santa_sample_phase": ([G, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
         "santa_bernoulli_scores": ([G, vp, vp, vp, i32, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),

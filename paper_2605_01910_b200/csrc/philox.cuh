@@ -6,7 +6,7 @@
 
 namespace santa {
 
-enum : uint32_t { kTagValueSampler = 1, kTagBernoulliHead = 2, kTagBernoulliGroup = 3, kTagPropTileOffset = 4 };
+enum : uint32_t { kTagValueSampler = 1, kTagBernoulliHead = 2, kTagBernoulliGroup = 3, kTagPropTileOffset = 4, kTagFlashTileOffset = 5 };
 
 struct Philox4 {
   uint32_t x[4];

@@ -130,13 +130,16 @@ __host__ __device__ inline size_t sample_smem_bytes(int Cmax, int S_local, int D
 // k = min{k : P_c[k] > sTl[m]} in the chunk's prefix block (ballots, L = 64; binary search
 // otherwise), writes idx_out[bh, m_lo + m], then loads and adds the V row; the half-warps'
 // sums are reduced in fixed order into sPart [D] (unscaled).  All threads call it.
-template <typename T, int D>
+// kW: each sample's row is scaled by sWt[m] (S^2ANTA-flash merge weights); idx rows are
+// idx_stride long (default S).
+template <typename T, int D, bool kW = false>
 __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
                                                   int Sl, int m_lo, int seqlen, const int* sChunk,
-                                                  const float* sTl, float* sRed, float* sPart) {
+                                                  const float* sTl, float* sRed, float* sPart,
+                                                  const float* sWt = nullptr, int idx_stride = -1) {
   const int NT = blockDim.x, NHW = NT >> 4;
   const int tid = threadIdx.x;
-  const int S = p.S;
+  const int S = idx_stride < 0 ? p.S : idx_stride;
   constexpr int EB = (int)sizeof(T);
   constexpr int VCH = D * EB / 16;                  // 16-B chunks per V row
   constexpr int NCH = (VCH + 15) / 16;              // chunks per lane
@@ -224,23 +227,31 @@ __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, 
         raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(vrow(jj[u]) + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
       }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U; ++u) {
+      float wt = 1.f;
+      if constexpr (kW) wt = jj[u] >= 0 ? sWt[m0 + u * NHW] : 0.f;
 #pragma unroll
       for (int q = 0; q < NCH; ++q) {
         if constexpr (EB == 2) {
           const uint32_t w[4] = {raw[u][q].x, raw[u][q].y, raw[u][q].z, raw[u][q].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            acc[q][2 * e] += Elem<T>::lo(w[e]);
-            acc[q][2 * e + 1] += Elem<T>::hi(w[e]);
+            if constexpr (kW) {
+              acc[q][2 * e] = fmaf(wt, Elem<T>::lo(w[e]), acc[q][2 * e]);
+              acc[q][2 * e + 1] = fmaf(wt, Elem<T>::hi(w[e]), acc[q][2 * e + 1]);
+            } else {
+              acc[q][2 * e] += Elem<T>::lo(w[e]);
+              acc[q][2 * e + 1] += Elem<T>::hi(w[e]);
+            }
           }
         } else {
-          acc[q][0] += __uint_as_float(raw[u][q].x);
-          acc[q][1] += __uint_as_float(raw[u][q].y);
-          acc[q][2] += __uint_as_float(raw[u][q].z);
-          acc[q][3] += __uint_as_float(raw[u][q].w);
+          acc[q][0] = fmaf(wt, __uint_as_float(raw[u][q].x), acc[q][0]);
+          acc[q][1] = fmaf(wt, __uint_as_float(raw[u][q].y), acc[q][1]);
+          acc[q][2] = fmaf(wt, __uint_as_float(raw[u][q].z), acc[q][2]);
+          acc[q][3] = fmaf(wt, __uint_as_float(raw[u][q].w), acc[q][3]);
         }
       }
+    }
   }
   SANTA_TRACE(9);  // V rows gathered and added (thread 0)
   // deterministic reduction over the half-warps (fixed order)
@@ -451,9 +462,10 @@ __device__ __forceinline__ void store_out(const SampleParams& p, size_t bh, int 
 // Sum the partials of the CS CTAs of one head's cluster (through DSMEM, fixed rank order), scale
 // by 1/S and store the head's output.
 template <typename T, int D>
-__device__ __forceinline__ void finish_head(const SampleParams& p, size_t bh, int rank, int CS, float* sPart) {
+__device__ __forceinline__ void finish_head(const SampleParams& p, size_t bh, int rank, int CS, float* sPart,
+                                            float scale = -1.f) {
   namespace cg = cooperative_groups;
-  const float invS = 1.0f / (float)p.S;
+  const float invS = scale >= 0.f ? scale : 1.0f / (float)p.S;
   if (CS > 1) {
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();

@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "dense_kernels.cuh"
 #include "dense_stream_kernel.cuh"
+#include "flash_kernels.cuh"
 #include "philox.cuh"
 #include "prop_kernels.cuh"
 #include "sample_kernels.cuh"
@@ -426,6 +427,62 @@ struct RunProp {
     return SANTA_OK;
   }
 };
+
+// S^2ANTA-flash per-tile draws + merge-weighted gather (flash_kernels.cuh), PDL-chained to the
+// score pass.  cpt = chunks per flash tile, mmax = idx row length (santa_flash_max_samples).
+template <typename T, int D, int G>
+struct RunFlash {
+  static santa_status run(const DecodeArgs& a, int cpt, int mmax) {
+    SampleParams p = make_sample_params(a);
+    int CS = 1;
+    const int heads = a.g->batch * a.g->n_heads;
+    // up to 4 CTAs per head within one wave (8-CTA clusters measured slower: 132 registers x 256
+    // threads fit one CTA per SM, so 256 CTAs ran in two waves)
+    while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= mmax) CS *= 2;
+    p.cluster = CS;
+    const size_t smem = flash_smem_bytes(p.Cmax, cpt, (mmax + CS - 1) / CS, D, kSampleThreads);
+    if (smem > 227 * 1024) return SANTA_ERR_UNSUPPORTED;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      if (cudaFuncSetAttribute(flash_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      configured = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
+    cfg.blockDim = dim3(kSampleThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    if (cudaLaunchKernelEx(&cfg, flash_gather_kernel<T, D, G>, p, cpt, mmax) != cudaSuccess) return SANTA_ERR_CUDA;
+    return SANTA_OK;
+  }
+};
+
+// idx row length of the flash path: max over sequence lengths <= max_seqlen of S_tile * T
+// (-1: tile_len is not a positive multiple of the chunk length, or more than 64 chunks).
+int flash_max_samples(const santa_geometry* g, int S, int tile_len, int* cpt_out) {
+  const int L = layout(g, 1).L;
+  if (tile_len < L || tile_len % L != 0 || tile_len / L > 64 || S < 1) return -1;
+  const int cpt = tile_len / L;
+  const int Tmax = (g->max_seqlen + tile_len - 1) / tile_len;
+  int mm = 0;
+  for (int T = 1; T <= Tmax; ++T) {
+    const int m = flash_tile_budget(T, S) * T;
+    if (m > mm) mm = m;
+  }
+  if (cpt_out) *cpt_out = cpt;
+  return mm;
+}
 
 // The whole step in one pipelined cooperative launch (step_kernel.cuh).  Returns
 // SANTA_ERR_UNSUPPORTED (nothing launched) when the configuration does not qualify, in which
@@ -908,6 +965,36 @@ santa_status santa_decode_attention_prop(const santa_geometry* g, const void* q,
 int32_t santa_prop_tile_len(const santa_geometry* g) {
   if (validate_geometry(g) != SANTA_OK) return -1;
   return layout(g, 1).L;
+}
+
+santa_status santa_decode_attention_flash(const santa_geometry* g, const void* q, const void* K, const void* V,
+                                          const int32_t* seqlens, int32_t S, int32_t tile_len, uint64_t seed,
+                                          uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
+                                          void* stream) {
+  santa_status s = validate_geometry(g);
+  if (s != SANTA_OK) return s;
+  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
+  if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
+  int cpt = 0;
+  const int mmax = flash_max_samples(g, S, tile_len, &cpt);
+  if (mmax < 0) return SANTA_ERR_INVALID_ARG;
+  if (mmax > 16384) return SANTA_ERR_UNSUPPORTED;
+  if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
+  if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 3u)) return SANTA_ERR_ALIGNMENT;
+  DecodeArgs a = {};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
+  a.g = g; a.q = q; a.K = K; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = SANTA_SYSTEMATIC;
+  a.seed = seed; a.offset = offset; a.out = out; a.idx_out = idx_out; a.ws = ws;
+  a.st = reinterpret_cast<cudaStream_t>(stream);
+  const int G = g->n_heads / g->n_kv_heads;
+  if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+  if ((s = dispatch<RunFlash>(g->dtype, g->head_dim, G, a, cpt, mmax)) != SANTA_OK) return s;
+  return last_cuda();
+}
+
+int32_t santa_flash_max_samples(const santa_geometry* g, int32_t S, int32_t tile_len) {
+  if (validate_geometry(g) != SANTA_OK) return -1;
+  return flash_max_samples(g, S, tile_len, nullptr);
 }
 
 santa_status santa_dense_reference(const santa_geometry* g, const void* q, const void* K, const void* V,
