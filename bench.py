@@ -685,8 +685,10 @@ def main():
         res["e2e"] = {"value": round(world * bytes_step / (ems * 1e-3) / 1e9, 2), "unit": "GB/s",
                       "us_per_step": round(ems * 1e3, 2),
                       "h2d_bytes_per_step": qkvh.numel() * 2, "d2h_bytes_per_step": outh.numel() * 2,
-                      "path": "santa_decode_step_host_packed: per step one pinned H2D of [q|k_new|v_new], KV append, "
-                              "decode, one D2H of out to pinned memory; back-to-back steps, CUDA events"}
+                      "path": "santa_decode_step_host_packed with pinned host buffers: per step the staging kernel "
+                              "reads [q|k_new|v_new] from pinned host memory (zero copy) and appends the KV rows, "
+                              "decode, the sampler writes out into pinned host memory; back-to-back steps, CUDA "
+                              "events"}
         # the synchronous single-call latency of the same API (host wall clock incl. the stream sync)
         et = []
         for i in range(args.warmup + args.steps):

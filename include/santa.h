@@ -312,6 +312,11 @@ santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_hos
  * (same size), then the KV append, santa_decode_attention, and one D2H of out_dev into out_host
  * (pinned, B*H*d).  synchronize != 0: syncs `stream` before returning (out_host is valid);
  * synchronize == 0: fully asynchronous, out_host is valid once the caller syncs the stream.
+ * Zero copy: a 16-B aligned PAGE-LOCKED qkv_host (cudaHostAlloc / cudaHostRegister) is read by the
+ * staging kernel itself (q rows -> qkv_dev, k/v rows -> the cache) and a page-locked out_host is
+ * written by the decode kernels themselves (out_dev then unused) -- no copy-engine transfers;
+ * pageable buffers use cudaMemcpyAsync.  The host must not modify qkv_host / read out_host
+ * before the stream reaches the end of this call's work.
  * Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
 santa_status santa_decode_step_host_packed(const santa_geometry* geo, const void* qkv_host, void* qkv_dev,
                                            void* K, void* V, const int32_t* seqlens, int32_t S,

@@ -199,10 +199,11 @@ def santa_decode_step_host(geo, q_host, k_new_host, v_new_host, q_dev, k_new_dev
 
 def santa_decode_step_host_packed(geo, qkv_host, qkv_dev, K, V, seqlens, S, mode, seed, offset, out_dev, out_host,
                                   ws, synchronize=True, stream=None):
-    """One H2D of the packed pinned [q | k_new | v_new] buffer, KV append, decode, one D2H of out."""
+    """Packed [q | k_new | v_new] host buffer -> KV append + decode -> out host buffer.  Pinned buffers
+    are read / written by the kernels (zero copy); pageable ones are copied (include/santa.h)."""
     for t in (qkv_host, out_host):
-        if t.is_cuda or not t.is_pinned():
-            raise ValueError("host buffers must be pinned CPU tensors")
+        if t.is_cuda or not t.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors")
     hp = lambda t: ctypes.c_void_p(t.data_ptr())  # noqa: E731
     _abi.check("santa_decode_step_host_packed", _abi.LIB.santa_decode_step_host_packed(
         ctypes.byref(geo), hp(qkv_host), _ptr(qkv_dev), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode),

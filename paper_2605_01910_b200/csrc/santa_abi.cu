@@ -723,6 +723,39 @@ __global__ void append_kv_kernel(void* K, void* V, const void* kn, const void* v
   }
 }
 
+// Zero-copy staging for the packed host API: one CTA per (b, kv head) reads its G query rows and
+// its new K/V rows straight from the PINNED host buffer (a device-addressable alias under UVA) with
+// 16-B loads, writes the q rows to the device staging buffer and the K/V rows into the cache slot
+// seqlens[b] - 1 -- the H2D copy and the append in one launch.
+__global__ void stage_append_kernel(const uint4* __restrict__ qkv_h, uint4* __restrict__ q_dev, void* K, void* V,
+                                    KvLayout kv, const int32_t* seqlens, int D, int eb, int G, int H) {
+  const int kvh = blockIdx.x, b = blockIdx.y, Hkv = kv.n_kv_heads;
+  const int row16 = D * eb / 16;                                 // 16-B words per row
+  const size_t q16 = (size_t)gridDim.y * H * row16, k16 = (size_t)gridDim.y * Hkv * row16;
+  const size_t qsrc = ((size_t)b * H + (size_t)kvh * G) * row16;
+  for (int i = threadIdx.x; i < G * row16; i += blockDim.x) q_dev[qsrc + i] = qkv_h[qsrc + i];
+  const int t = __ldg(seqlens + b) - 1;
+  if (t < 0) return;
+  const int64_t dst16 = kv.row(b, kvh, t, D) * eb / 16;
+  const size_t ksrc = q16 + ((size_t)b * Hkv + kvh) * row16;
+  for (int i = threadIdx.x; i < row16; i += blockDim.x) {
+    reinterpret_cast<uint4*>(K)[dst16 + i] = qkv_h[ksrc + i];
+    reinterpret_cast<uint4*>(V)[dst16 + i] = qkv_h[ksrc + k16 + i];
+  }
+}
+
+// The device-addressable alias of a page-locked host pointer (cudaHostAlloc / cudaHostRegister,
+// e.g. torch pin_memory), or NULL for pageable memory.  Queried per call (no cache: a freed pinned
+// buffer's address can come back as pageable memory).
+const void* pinned_alias(const void* hp) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, hp) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
 __global__ void philox_test_kernel(uint64_t seed, uint64_t offset, uint32_t tag, uint32_t h, uint32_t b, int n,
                                    double* out, uint4 ctr, uint2 key, uint32_t* raw) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1152,14 +1185,25 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
   const size_t qb = (size_t)g->batch * g->n_heads * D * eb, kb = (size_t)g->batch * g->n_kv_heads * D * eb;
   if ((qb % 16) || (kb % 16)) return SANTA_ERR_ALIGNMENT;  // k_new / v_new sub-buffers stay 16-B aligned
   char* dev = reinterpret_cast<char*>(qkv_dev);
-  if (cudaMemcpyAsync(dev, qkv_host, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
-  append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, dev + qb, dev + qb + kb, kv_layout(g), seqlens,
-                                                                  (int)D, (int)eb);
+  // pinned host buffers are read / written by the kernels themselves (zero copy: no copy-engine
+  // round trips); pageable ones go through cudaMemcpyAsync
+  const void* qkv_alias = aligned16(qkv_host) ? pinned_alias(qkv_host) : nullptr;
+  void* out_alias = aligned16(out_host) ? const_cast<void*>(pinned_alias(out_host)) : nullptr;
+  if (qkv_alias) {
+    stage_append_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(
+        reinterpret_cast<const uint4*>(qkv_alias), reinterpret_cast<uint4*>(dev), K, V, kv_layout(g), seqlens, (int)D,
+        (int)eb, g->n_heads / g->n_kv_heads, g->n_heads);
+  } else {
+    if (cudaMemcpyAsync(dev, qkv_host, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
+    append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, dev + qb, dev + qb + kb, kv_layout(g),
+                                                                    seqlens, (int)D, (int)eb);
+  }
   if ((s = last_cuda()) != SANTA_OK) return s;
-  if ((s = decode_common(g, dev, K, V, seqlens, S, mode, seed, offset, out_dev, nullptr, ws, ws_bytes, nullptr,
-                         stream)) != SANTA_OK)
+  if ((s = decode_common(g, dev, K, V, seqlens, S, mode, seed, offset, out_alias ? out_alias : out_dev, nullptr, ws,
+                         ws_bytes, nullptr, stream)) != SANTA_OK)
     return s;
-  if (cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (!out_alias && cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return SANTA_ERR_CUDA;
   if (synchronize && cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
   return SANTA_OK;
 }

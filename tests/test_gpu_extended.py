@@ -151,9 +151,11 @@ def test_decode_step_host_matches_device_call():
     assert torch.equal(outh, ref.cpu())
 
 
-def test_decode_step_host_packed_async_matches_device_call():
-    """The packed-buffer host API (one H2D, append, decode, one D2H), asynchronous over several
-    steps, gives for every step exactly the device call's output on the appended cache."""
+@pytest.mark.parametrize("pinned", [True, False])
+def test_decode_step_host_packed_async_matches_device_call(pinned):
+    """The packed-buffer host API (zero-copy staging from pinned buffers, or H2D + append + D2H
+    copies for pageable ones), asynchronous over several steps, gives for every step exactly the
+    device call's output on the appended cache."""
     B, H, Hkv, d, S = 2, 16, 4, 128, 64
     n = [700, 1500]
     inp = to_cuda(si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=33, max_seqlen=1600))
@@ -161,8 +163,9 @@ def test_decode_step_host_packed_async_matches_device_call():
     ws = santa.workspace(geo, S)
     K2, V2 = inp.K.clone(), inp.V.clone()
     steps = 3
-    qkvs = [torch.randn(B * H * d + 2 * B * Hkv * d).to(torch.bfloat16).pin_memory() for _ in range(steps)]
-    outs = [torch.empty(B * H * d, dtype=torch.bfloat16).pin_memory() for _ in range(steps)]
+    pin = (lambda t: t.pin_memory()) if pinned else (lambda t: t)  # noqa: E731
+    qkvs = [pin(torch.randn(B * H * d + 2 * B * Hkv * d).to(torch.bfloat16)) for _ in range(steps)]
+    outs = [pin(torch.empty(B * H * d, dtype=torch.bfloat16)) for _ in range(steps)]
     devbufs = [torch.empty(B * H * d + 2 * B * Hkv * d, dtype=torch.bfloat16, device="cuda") for _ in range(steps)]
     od = [torch.empty_like(inp.q) for _ in range(steps)]
     for i in range(steps):
@@ -184,3 +187,26 @@ def test_decode_step_host_packed_async_matches_device_call():
         assert torch.equal(outs[i], ref.reshape(-1).cpu()), i
         if i == steps - 1:
             assert torch.equal(K2, K3) and torch.equal(V2, V3)
+
+
+def test_prop_and_flash_batch_slabs_equal_full_run():
+    """The batch x kv-head sharding of bench.py applies to S^2ANTA-prop and -flash too: their a0
+    streams are keyed by global (b, h), so every slab reproduces the full run bit for bit."""
+    B, H, Hkv, d = 3, 16, 4, 128
+    inp = to_cuda(si.make_decode_inputs(B, H, Hkv, d, [700, 1200, 333], dtype="bf16", seed=34))
+    G = H // Hkv
+    pf_out, pf_idx = santa.decode_prop(inp.q, inp.K, inp.V, inp.seqlens, 96, seed=9, return_idx=True)
+    ff_out, ff_idx = santa.decode_flash(inp.q, inp.K, inp.V, inp.seqlens, 256, 128, seed=9, return_idx=True)
+    torch.cuda.synchronize()
+    for slabs in sharding.plan_units(B, Hkv, 3):
+        for slab in slabs:
+            qs, Ks, Vs, sl = sharding.slab_inputs(inp.q, inp.K, inp.V, inp.seqlens, slab, G)
+            sel = (slice(slab.b0, slab.b1), slice(slab.k0 * G, slab.k1 * G))
+            out, idx = santa.decode_prop(qs, Ks, Vs, sl, 96, seed=9, return_idx=True, batch_offset=slab.b0,
+                                         head_offset=slab.k0 * G, max_seqlen=inp.K.shape[2])
+            torch.cuda.synchronize()
+            assert torch.equal(out, pf_out[sel]) and torch.equal(idx, pf_idx[sel])
+            out, idx = santa.decode_flash(qs, Ks, Vs, sl, 256, 128, seed=9, return_idx=True, batch_offset=slab.b0,
+                                          head_offset=slab.k0 * G, max_seqlen=inp.K.shape[2])
+            torch.cuda.synchronize()
+            assert torch.equal(out, ff_out[sel]) and torch.equal(idx, ff_idx[sel])
