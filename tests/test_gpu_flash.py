@@ -189,3 +189,19 @@ def test_flash_unbiased_gpu():
     exact = o.dense_decode(si.as_bits(inp.q), si.as_bits(inp.K), si.as_bits(inp.V), [2048])
     z = np.abs(mean - exact) / np.maximum(se, 1e-6)
     assert np.mean(z > 4) < 0.01 and np.abs(mean - exact).max() < 0.05
+
+
+@pytest.mark.parametrize("n", [300_001, 600_000])
+def test_prop_and_flash_long_context(n):
+    """Long contexts: 4688 / 9375 score chunks per sequence; beyond 512k tokens the chunk (and so
+    prop's tile) is 128 keys.  Both estimators against the oracle on one GQA group."""
+    from test_gpu_prop import prop_parity
+    inp = to_cuda(si.make_decode_inputs(1, 4, 1, 128, n, dtype="bf16", seed=40, workload="temp4"))
+    geo = santa.make_geometry(inp.q, 1, n)
+    tile = santa.santa_prop_tile_len(geo)
+    assert tile == (64 if n <= 524288 else 128)
+    out, idx = santa.decode_prop(inp.q, inp.K, inp.V, inp.seqlens, 1024, seed=3, return_idx=True)
+    torch.cuda.synchronize()
+    prop_parity(inp, out, idx, 1024, 3, B_tile=tile)
+    out, idx = gpu_flash(inp, 2048, 512, seed=3)
+    flash_parity(inp, out, idx, 2048, 512, 3)
