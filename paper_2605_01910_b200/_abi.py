@@ -8,7 +8,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsanta.so")
+LIB_PATH = os.environ.get("SANTA_LIB_PATH") or os.path.join(_HERE, "_lib", "libsanta.so")  # override: A/B builds (tools/)
 
 SANTA_OK = 0
 STATUS = {0: "SANTA_OK", 1: "SANTA_ERR_INVALID_ARG", 2: "SANTA_ERR_SHAPE", 3: "SANTA_ERR_EMPTY_BUDGET",
