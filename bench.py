@@ -96,6 +96,11 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's NVML start-up (tens of ms) must not overlap the ~1 ms timed loop: wait for
+            # its first sample; it keeps sampling every 50 ms through the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.005)
         except FileNotFoundError:
             self.proc = None
         return self

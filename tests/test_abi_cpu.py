@@ -112,3 +112,25 @@ def test_auto_path_policy_is_host_logic():
     assert santa.santa_auto_path(_geo(batch=32, max_seqlen=131072), 256) == "two_kernel"
     with pytest.raises(santa.SantaError):
         santa.santa_auto_path(_geo(max_seqlen=0), 256)
+
+
+def test_prop_and_flash_host_logic():
+    """S^2ANTA-prop / -flash entry points: tile length, flash idx row length (max over sequence lengths
+    of S_tile * T, against the oracle's S_tile rule) and argument rejection -- all before any launch."""
+    from oracle import santa_oracle as o
+    L = _abi.LIB
+    for n, tile in ((32768, 64), (524288, 64), (524289, 128), (1 << 20, 128)):
+        g = _geo(max_seqlen=n)
+        assert L.santa_prop_tile_len(ctypes.byref(g)) == tile
+    g = _geo(max_seqlen=32768)
+    for S, tile in ((2048, 256), (256, 64), (1, 1024), (7, 128)):
+        want = max(o.flash_tile_budget(T * tile, tile, S) * T for T in range(1, 32768 // tile + 1))
+        assert L.santa_flash_max_samples(ctypes.byref(g), S, tile) == want
+    for bad in (0, 32, 96, 64 * 65):
+        assert L.santa_flash_max_samples(ctypes.byref(g), 64, bad) == -1
+    a = (16, 16, 16, 16)
+    assert L.santa_decode_attention_prop(ctypes.byref(g), *a, 0, 0, 0, 16, None, 256, 1 << 30, None) == 3
+    assert L.santa_decode_attention_prop(ctypes.byref(g), None, 16, 16, 16, 8, 0, 0, 16, None, 256, 1 << 30,
+                                         None) == 1
+    assert L.santa_decode_attention_flash(ctypes.byref(g), *a, 8, 100, 0, 0, 16, None, 256, 1 << 30, None) == 1
+    assert L.santa_decode_attention_flash(ctypes.byref(g), *a, 0, 256, 0, 0, 16, None, 256, 1 << 30, None) == 3
