@@ -132,11 +132,11 @@ __host__ __device__ inline size_t sample_smem_bytes(int Cmax, int S_local, int D
 // sums are reduced in fixed order into sPart [D] (unscaled).  All threads call it.
 // kW: each sample's row is scaled by sWt[m] (S^2ANTA-flash merge weights); idx rows are
 // idx_stride long (default S).
-template <typename T, int D, bool kW = false>
-__device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
-                                                  int Sl, int m_lo, int seqlen, const int* sChunk,
-                                                  const float* sTl, float* sRed, float* sPart,
-                                                  const float* sWt = nullptr, int idx_stride = -1) {
+template <typename T, int D, bool kW, int U>
+__device__ __forceinline__ void gather_chunk_rows_u(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
+                                                    int Sl, int m_lo, int seqlen, const int* sChunk,
+                                                    const float* sTl, float* sRed, float* sPart, const float* sWt,
+                                                    int idx_stride) {
   const int NT = blockDim.x, NHW = NT >> 4;
   const int tid = threadIdx.x;
   const int S = idx_stride < 0 ? p.S : idx_stride;
@@ -144,7 +144,6 @@ __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, 
   constexpr int VCH = D * EB / 16;                  // 16-B chunks per V row
   constexpr int NCH = (VCH + 15) / 16;              // chunks per lane
   constexpr int EPC = 16 / EB;                      // elements per chunk
-  constexpr int U = 8;                              // samples in flight per half-warp
   const int hw = tid >> 4, l = tid & 15;
   const unsigned hmask = 0xffffu << (threadIdx.x & 16);
   float acc[NCH][EPC];
@@ -270,6 +269,23 @@ __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, 
     sPart[d] = s;
   }
   __syncthreads();
+}
+
+// U = samples in flight per half-warp.  U = 4 when one pass covers the work item (config 2: 4 per
+// half-warp): the unrolled U = 8 body is twice the code, half of it predicated off, and its
+// instruction fetch was the kernel's top stall (ncu `no_instructions` 52 %; sample phase 9.1 -> 8.1
+// us); U = 8 otherwise (flash at S = 2048: 36.9 vs 40.6 us with U = 4).
+template <typename T, int D, bool kW = false>
+__device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
+                                                  int Sl, int m_lo, int seqlen, const int* sChunk,
+                                                  const float* sTl, float* sRed, float* sPart,
+                                                  const float* sWt = nullptr, int idx_stride = -1) {
+  if (Sl <= 4 * (int)(blockDim.x >> 4))
+    gather_chunk_rows_u<T, D, kW, 4>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, sWt,
+                                     idx_stride);
+  else
+    gather_chunk_rows_u<T, D, kW, 8>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, sWt,
+                                     idx_stride);
 }
 
 // One (b, h, split) work item.  Leaves the CTA's partial sum sum_{own m} V_{J_m} (fp32, not yet
