@@ -836,9 +836,15 @@ santa_status validate_bern(const santa_geometry* g, const void* q, const void* K
 }
 
 int auto_path(const santa_geometry* g, int S) {
-  const bool step_ok = g->dtype != SANTA_F32 && g->max_seqlen <= 65536 &&
-                       (!g->page_table || g->page_size % kTcTileKeys == 0);
-  if (step_ok && (int64_t)g->batch * g->n_heads >= kTcMinHeads && S <= 256) return SANTA_PATH_STEP_TC;
+  const bool step_ok = g->dtype != SANTA_F32 && g->max_seqlen <= 65536;
+  const bool tc_pages = !g->page_table || g->page_size % kTcTileKeys == 0;
+  if (step_ok && (int64_t)g->batch * g->n_heads >= kTcMinHeads) {
+    // batch 32 (tools/path_sweep.py, profiles/r01_v10_path_sweep_*.json): S <= 256 the tcgen05 step
+    // kernel (367 / 383-393 us at S = 64 / 256), S = 512 the mma.sync step kernel (419 vs 437 us for
+    // the two-kernel path, 458 for tcgen05)
+    if (S <= 256 && tc_pages) return SANTA_PATH_STEP_TC;
+    if (S > 256 && S <= 512) return SANTA_PATH_STEP_KERNEL;
+  }
   return SANTA_PATH_TWO_KERNEL;
 }
 

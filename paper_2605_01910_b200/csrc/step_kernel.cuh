@@ -755,7 +755,9 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
     }
   } else if constexpr ((kVar & 2) == 0) {
     // ---------------- sampler group ----------------
-    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag8);
+    // 4 samples in flight per half-warp (tools/path_sweep.py, batch 32: S = 256 403 -> 395 us,
+    // S = 512 435 -> 419 us; the tcgen05 kernel keeps 8: its S = 64 / 512 points got slower)
+    step_sampler_loop<T, D, G, NSW, 4>(sp, sy, samp_smem, tag32, tag8);
   }
   // ---------------- exit ticket: the last CTA out advances the epoch ----------------
   __syncthreads();
