@@ -8,8 +8,10 @@
  * Conventions shared by every entry point
  * ---------------------------------------
  * - All tensor pointers are DEVICE pointers unless the name ends in _host.  The
- *   caller owns every buffer; the library never allocates or frees device memory
- *   and keeps no global mutable state (calls on different streams are reentrant).
+ *   caller owns every buffer; the library never allocates or frees device memory.
+ *   Its only process-wide state is a cache of per-(kernel, device) launch attributes
+ *   and per-device SM counts, guarded by a mutex and written idempotently, so calls
+ *   from several host threads on different streams (and devices) are reentrant.
  * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
  *   Calls are stream-ordered and asynchronous: a return of SANTA_OK means the
  *   work was launched, not that it finished.
@@ -162,8 +164,10 @@ int32_t santa_auto_path(const santa_geometry* geo, int32_t S);
 
 /* santa_decode_attention with an explicit execution path (santa_path: AUTO, STEP_KERNEL,
  * TWO_KERNEL, STEP_TC); AUTO is exactly santa_decode_attention.  A forced path that does not
- * support the geometry (e.g. a step kernel on an fp32 cache) returns SANTA_ERR_UNSUPPORTED and
- * launches nothing.  Used by the tests and bench.py to compare the paths. */
+ * support the geometry returns SANTA_ERR_UNSUPPORTED and launches nothing: the step kernels
+ * (STEP_KERNEL, STEP_TC) need a bf16/fp16 cache, contiguous or pages of a multiple of 64 (STEP_TC:
+ * 128) tokens, and max_seqlen <= 65536 (their sampler keeps <= 1024 chunk statistics per head in
+ * registers).  Used by the tests and bench.py to compare the paths. */
 santa_status santa_decode_attention_path(const santa_geometry* geo, const void* q, const void* K,
                                          const void* V, const int32_t* seqlens, int32_t S,
                                          int32_t mode, uint64_t seed, uint64_t offset, void* out,
@@ -297,7 +301,9 @@ santa_status santa_seqshard_sample_gather(const santa_geometry* geo, const doubl
  * into the device staging buffers q_dev / k_new_dev / v_new_dev, appends k_new / v_new to
  * the cache at position seqlens[b]-1 (the "+1 slot"), runs
  * santa_decode_attention into out_dev and copies it to out_host; synchronises `stream`
- * before returning.  Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
+ * before returning.  Every check of santa_decode_attention runs BEFORE the first copy or launch,
+ * so an invalid call leaves the cache untouched.
+ * Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
 santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_host,
                                     const void* k_new_host, const void* v_new_host,
                                     void* q_dev, void* k_new_dev, void* v_new_dev, void* K,
@@ -315,7 +321,8 @@ santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_hos
  * Zero copy: a 16-B aligned PAGE-LOCKED qkv_host (cudaHostAlloc / cudaHostRegister) is read by the
  * staging kernel itself (q rows -> qkv_dev, k/v rows -> the cache) and a page-locked out_host is
  * written by the decode kernels themselves (out_dev then unused) -- no copy-engine transfers;
- * pageable buffers use cudaMemcpyAsync.  The host must not modify qkv_host / read out_host
+ * pageable buffers use cudaMemcpyAsync.  All argument checks run before the first copy or launch
+ * (an invalid call leaves the cache untouched).  The host must not modify qkv_host / read out_host
  * before the stream reaches the end of this call's work.
  * Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
 santa_status santa_decode_step_host_packed(const santa_geometry* geo, const void* qkv_host, void* qkv_dev,

@@ -14,8 +14,12 @@ SPEC.md; "reading #k" = the k-th interpretation listed in DESIGN.md sec. 2.
 Parity status: every public function below is pinned by a ``-m "not gpu"``
 test in tests/test_oracle_*.py against something other than itself (Random123
 known-answer vectors, the paper's worked example, closed forms, brute force,
-exact-law enumeration, the paper's printed Bernoulli error figures).  No
-function here is "parity unpinned".
+exact-law enumeration, the paper's printed Bernoulli error figures).  The
+validity machinery every GPU verdict rests on -- ``index_mismatch_report``
+(the 1e-6 exemption rule), ``santa_from_scores`` and the per-head branch of
+``bernoulli_scores`` -- is pinned in tests/test_oracle_validity.py on hand-built
+cases with hand-derived verdicts.  No function here is "parity unpinned"
+(audit: every ``def`` is called by name from a tests/test_oracle_*.py file).
 """
 from __future__ import annotations
 

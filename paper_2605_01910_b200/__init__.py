@@ -226,12 +226,35 @@ def santa_read_error_flags(ws, stream=None) -> int:
 
 # ---- convenience wrappers (allocation + the call; still no compute in Python) ----------------
 
+def _check_cache(q, K, V, Hkv, n_max, page_table, page_size):
+    """Shape/dtype agreement between q and the cache the geometry will describe.  For a contiguous
+    cache the row stride of K and V IS max_seqlen (santa.h), so a max_seqlen different from
+    K.shape[2] would silently read the wrong rows: refuse it."""
+    if q.dim() != 3:
+        raise ValueError(f"q must be [B, H, d], got {tuple(q.shape)}")
+    B, H, d = q.shape
+    if K.dtype != q.dtype or V.dtype != q.dtype:
+        raise ValueError(f"q, K, V must share a dtype (got {q.dtype}, {K.dtype}, {V.dtype})")
+    if K.shape != V.shape:
+        raise ValueError(f"K and V shapes differ: {tuple(K.shape)} vs {tuple(V.shape)}")
+    if page_table is None:
+        if tuple(K.shape) != (B, Hkv, n_max, d):
+            raise ValueError(f"contiguous cache must be [B, H_kv, max_seqlen, d] = {(B, Hkv, n_max, d)}, "
+                             f"got {tuple(K.shape)}")
+    else:
+        if K.dim() != 4 or K.shape[1] != Hkv or K.shape[2] != page_size or K.shape[3] != d:
+            raise ValueError(f"paged pool must be [pages, H_kv, page_size, d] = [*, {Hkv}, {page_size}, {d}], "
+                             f"got {tuple(K.shape)}")
+        if page_table.dtype != torch.int32 or page_table.dim() != 2 or page_table.shape[0] != B:
+            raise ValueError("page_table must be int32 [B, max_pages_per_seq]")
+
 def decode(q, K, V, seqlens, S, mode="stratified", seed=0, offset=0, n_kv_heads=None, page_table=None,
            page_size=0, max_seqlen=None, return_idx=False, ws=None, batch_offset=0, head_offset=0, path="auto"):
     """Allocate out (+ idx) and workspace, run santa_decode_attention.  K/V are either the
     contiguous [B, H_kv, n_max, d] cache or the paged pool [pages, H_kv, P, d]."""
     Hkv = n_kv_heads or K.shape[1]
     n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    _check_cache(q, K, V, Hkv, n_max, page_table, page_size)
     geo = make_geometry(q, Hkv, n_max, page_table, page_size, batch_offset=batch_offset, head_offset=head_offset)
     if ws is None:
         ws = workspace(geo, S, q.device)
@@ -246,6 +269,7 @@ def decode_prop(q, K, V, seqlens, S, seed=0, offset=0, n_kv_heads=None, page_tab
     """Allocate out (+ idx) and workspace, run santa_decode_attention_prop (S^2ANTA-prop)."""
     Hkv = n_kv_heads or K.shape[1]
     n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    _check_cache(q, K, V, Hkv, n_max, page_table, page_size)
     geo = make_geometry(q, Hkv, n_max, page_table, page_size, batch_offset=batch_offset, head_offset=head_offset)
     if ws is None:
         ws = workspace(geo, S, q.device)
@@ -260,6 +284,7 @@ def decode_flash(q, K, V, seqlens, S, tile_len=256, seed=0, offset=0, n_kv_heads
     """Allocate out (+ idx [B, H, santa_flash_max_samples]) and workspace, run santa_decode_attention_flash."""
     Hkv = n_kv_heads or K.shape[1]
     n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    _check_cache(q, K, V, Hkv, n_max, page_table, page_size)
     geo = make_geometry(q, Hkv, n_max, page_table, page_size, batch_offset=batch_offset, head_offset=head_offset)
     if ws is None:
         ws = workspace(geo, S, q.device)
@@ -275,6 +300,7 @@ def decode_flash(q, K, V, seqlens, S, tile_len=256, seed=0, offset=0, n_kv_heads
 def dense(q, K, V, seqlens, n_kv_heads=None, page_table=None, page_size=0, max_seqlen=None, ws=None):
     Hkv = n_kv_heads or K.shape[1]
     n_max = max_seqlen or (K.shape[2] if page_table is None else page_table.shape[1] * page_size)
+    _check_cache(q, K, V, Hkv, n_max, page_table, page_size)
     geo = make_geometry(q, Hkv, n_max, page_table, page_size)
     if ws is None:
         ws = workspace(geo, 1, q.device)

@@ -1,8 +1,12 @@
 // santa_abi.cu -- host side of libsanta.so: argument validation, workspace layout,
 // template dispatch and (PDL-chained) launches.  See include/santa.h for the contract.
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include <cudaTypedefs.h>
 
@@ -190,28 +194,86 @@ struct DecodeArgs {
   bool tensor_core = false;   // step kernel: score stage on tcgen05 (step_tc_kernel.cuh)
 };
 
-int num_sms() {
-  static int cached[64] = {0};
+// ---- host-side caches: per device, safe under concurrent calls from several host threads ----
+// (santa.h promises reentrancy: the only process-wide state is these caches of facts about the
+// device and the kernels, each written idempotently.)
+constexpr int kMaxDevices = 64;
+
+int current_device() {
   int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return 148;
-  if (!cached[dev]) {
-    int n = 0;
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cached[dev] = n > 0 ? n : 148;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
   }
-  return cached[dev];
+  return dev;
+}
+
+int num_sms() {
+  static std::atomic<int> cached[kMaxDevices];  // zero-initialised (static storage)
+  const int dev = current_device();
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  int n = cached[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = 148;
+    }
+    cached[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per (kernel, device): remember the largest
+// value set for each pair.  Two threads racing on a first call both set the attribute (idempotent).
+std::mutex g_attr_mu;
+
+template <typename Kern>
+cudaError_t ensure_smem(Kern kern, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  static std::map<std::pair<const void*, int>, size_t> cache;  // guarded by g_attr_mu
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), current_device());
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = cache.find(key);
+    if (it != cache.end() && it->second >= smem) return cudaSuccess;
+  }
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  size_t& v = cache[key];
+  if (v < smem) v = smem;
+  return cudaSuccess;
+}
+
+// Can a persistent kernel keep one CTA per SM at this block size and smem?  Cached per (kernel,
+// device, smem): the host-side cost per call matters at ~15-25 us per step.
+template <typename Kern>
+bool fits_one_per_sm(Kern kern, int nthreads, size_t smem) {
+  static std::map<std::pair<std::pair<const void*, int>, size_t>, bool> cache;  // guarded by g_attr_mu
+  const auto key = std::make_pair(std::make_pair(reinterpret_cast<const void*>(kern), current_device()), smem);
+  {
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  int occ = 0;
+  const bool r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nthreads, smem) == cudaSuccess && occ >= 1;
+  if (!r) cudaGetLastError();
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  cache[key] = r;
+  return r;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = []() -> PFN_cuTensorMapEncodeTiled_v12000 {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    cudaGetLastError();
+    return nullptr;
+  }();  // C++11 function-local static: initialised once, thread-safe
   return fn;
 }
 
@@ -280,13 +342,7 @@ struct RunScore {
       constexpr int NW = kStreamWarps, SPW = kStreamSlots;
       const size_t smem = 1024 + (size_t)NW * G * p.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
       if (smem <= 220 * 1024) {  // else: per-warp score buffers too large (G * L big) -> fallback kernel
-      static size_t configured = 0;
-      if (smem > configured) {
-        if (cudaFuncSetAttribute(score_stream_kernel<T, D, G, NW, SPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-          return SANTA_ERR_CUDA;
-        configured = smem;
-      }
+      if (ensure_smem(score_stream_kernel<T, D, G, NW, SPW>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
       const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
       const int grid = total < num_sms() ? total : num_sms();
       if (launch(score_stream_kernel<T, D, G, NW, SPW>, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p) !=
@@ -298,13 +354,7 @@ struct RunScore {
     {
       dim3 grid(a.L.Cmax, a.g->n_kv_heads, a.g->batch);
       const size_t smem = (size_t)G * p.L * 4;
-      static size_t configured = 0;
-      if (smem > 48 * 1024 && smem > configured) {
-        if (cudaFuncSetAttribute(score_chunk_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem) != cudaSuccess)
-          return SANTA_ERR_CUDA;
-        configured = smem;
-      }
+      if (ensure_smem(score_chunk_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
       if (launch(score_chunk_kernel<T, D, G>, grid, dim3(128), smem, a.st, false, p) != cudaSuccess)
         return SANTA_ERR_CUDA;
     }
@@ -356,13 +406,7 @@ struct RunSample {
     while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
     p.cluster = CS;
     const size_t smem = sample_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(sample_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return SANTA_ERR_CUDA;
-      configured = smem;
-    }
+    if (ensure_smem(sample_gather_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
     if (a.events) cudaEventRecord(a.events[1], a.st);
     const bool pdl = a.events == nullptr && a.stats_all == nullptr;
     cudaLaunchConfig_t cfg = {};
@@ -402,13 +446,7 @@ struct RunProp {
     p.cluster = CS;
     const size_t smem = prop_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
     if (smem > 227 * 1024) return SANTA_ERR_UNSUPPORTED;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(prop_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return SANTA_ERR_CUDA;
-      configured = smem;
-    }
+    if (ensure_smem(prop_gather_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
     cfg.blockDim = dim3(kSampleThreads);
@@ -442,13 +480,7 @@ struct RunFlash {
     p.cluster = CS;
     const size_t smem = flash_smem_bytes(p.Cmax, cpt, (mmax + CS - 1) / CS, D, kSampleThreads);
     if (smem > 227 * 1024) return SANTA_ERR_UNSUPPORTED;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-      if (cudaFuncSetAttribute(flash_gather_kernel<T, D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem) != cudaSuccess)
-        return SANTA_ERR_CUDA;
-      configured = smem;
-    }
+    if (ensure_smem(flash_gather_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
     cfg.blockDim = dim3(kSampleThreads);
@@ -523,15 +555,8 @@ struct RunStep {
       const size_t smem = step_tc_score_smem_bytes(D, G) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
       if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;
       auto kern = santa_step_tc_kernel<T, D, G, NSW>;
-      static size_t configured = 0;
-      if (smem > configured) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-          return SANTA_ERR_CUDA;
-        int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
-          return SANTA_ERR_UNSUPPORTED;
-        configured = smem;
-      }
+      if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+      if (!fits_one_per_sm(kern, NT, smem)) return SANTA_ERR_UNSUPPORTED;
       CUtensorMap tk, tq;
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
@@ -559,6 +584,8 @@ struct RunStep {
       return SANTA_ERR_UNSUPPORTED;
     } else {
       if (!stream_eligible(a.g) || a.L.L != kStepStageKeys) return SANTA_ERR_UNSUPPORTED;
+      // the sampler group's chunk-CDF registers hold <= kStepMaxChunks chunks (65,536 tokens)
+      if (a.L.Cmax > kStepMaxChunks) return SANTA_ERR_UNSUPPORTED;
       constexpr int NW = kStepConsumers, SPW = kStepSlots, NSW = kStepSamplers, NT = 32 * (NW + 1 + NSW);
       ScoreParams sp = make_score_params(a);
       SampleParams pp = make_sample_params(a);
@@ -574,19 +601,8 @@ struct RunStep {
       const size_t smem = step_score_smem_bytes(D, G, NW, SPW) + step_sample_smem_bytes(pp.Cmax, (a.S + CS - 1) / CS, D);
       if (smem > 226 * 1024) return SANTA_ERR_UNSUPPORTED;  // 227 KiB per CTA minus static smem
       auto kern = santa_step_kernel<T, D, G, NW, SPW, NSW>;
-      static size_t configured = 0;
-      if (smem > configured) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-          return SANTA_ERR_CUDA;
-        configured = smem;
-      }
-      static size_t occ_checked = 0;  // host-side per-call cost matters at ~25 us per step: query once per size
-      if (smem > occ_checked) {
-        int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem) != cudaSuccess || occ < 1)
-          return SANTA_ERR_UNSUPPORTED;
-        occ_checked = smem;
-      }
+      if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+      if (!fits_one_per_sm(kern, NT, smem)) return SANTA_ERR_UNSUPPORTED;
       CUtensorMap tm;
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
@@ -631,13 +647,7 @@ struct RunDense {
         constexpr int NW = kDenseWarps, SPW = kDenseSlots;
         constexpr size_t kStageBytes = 2 * (D / 64) * kDenseStageKeys * 128;
         const size_t smem = 1024 + (size_t)NW * SPW * (kStageBytes + 16) + (size_t)NW * 8 * kPRow * 2;
-        static size_t configured = 0;
-        if (smem > configured) {
-          if (cudaFuncSetAttribute(dense_stream_kernel<T, D, G, NW, SPW>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return SANTA_ERR_CUDA;
-          configured = smem;
-        }
+        if (ensure_smem(dense_stream_kernel<T, D, G, NW, SPW>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
         CUtensorMap tk, tv;
         const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                               : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
@@ -848,33 +858,40 @@ int auto_path(const santa_geometry* g, int S) {
   return SANTA_PATH_TWO_KERNEL;
 }
 
-santa_status decode_common(const santa_geometry* g, const void* q, const void* K, const void* V,
-                           const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
-                           void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
-                           void* stream, int path = SANTA_PATH_AUTO) {
+// Every check santa_decode_attention makes, with no side effect: fills *a on success.  The host-buffer
+// entry points call it BEFORE their first copy or launch (santa.h: on any error nothing is launched).
+santa_status prepare_decode(const santa_geometry* g, const void* q, const void* K, const void* V,
+                            const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
+                            void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
+                            void* stream, int path, DecodeArgs* a) {
   santa_status s = validate_geometry(g);
-  if (path < SANTA_PATH_AUTO || path > SANTA_PATH_STEP_TC) return SANTA_ERR_INVALID_ARG;
-  const bool auto_requested = path == SANTA_PATH_AUTO;
   if (s != SANTA_OK) return s;
+  if (path < SANTA_PATH_AUTO || path > SANTA_PATH_STEP_TC) return SANTA_ERR_INVALID_ARG;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
   if (S > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
   if (mode < SANTA_IID || mode > SANTA_SYSTEMATIC) return SANTA_ERR_INVALID_ARG;
   if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
   if (idx_out && (reinterpret_cast<uintptr_t>(idx_out) & 3u)) return SANTA_ERR_ALIGNMENT;
-  DecodeArgs a = {};
-  if ((s = check_ws(g, S, ws, ws_bytes, &a.L)) != SANTA_OK) return s;
-  a.g = g; a.q = q; a.K = K; a.V = V; a.seqlens = seqlens; a.S = S; a.mode = mode;
-  a.seed = seed; a.offset = offset; a.out = out; a.idx_out = idx_out; a.ws = ws;
-  a.st = reinterpret_cast<cudaStream_t>(stream);
-  a.events = reinterpret_cast<cudaEvent_t const*>(events);
+  *a = DecodeArgs{};
+  if ((s = check_ws(g, S, ws, ws_bytes, &a->L)) != SANTA_OK) return s;
+  a->g = g; a->q = q; a->K = K; a->V = V; a->seqlens = seqlens; a->S = S; a->mode = mode;
+  a->seed = seed; a->offset = offset; a->out = out; a->idx_out = idx_out; a->ws = ws;
+  a->st = reinterpret_cast<cudaStream_t>(stream);
+  a->events = reinterpret_cast<cudaEvent_t const*>(events);
+  return SANTA_OK;
+}
+
+// Launch a prepared decode step on `path` (AUTO resolved here).
+santa_status run_decode(DecodeArgs& a, int path) {
+  const santa_geometry* g = a.g;
+  const bool auto_requested = path == SANTA_PATH_AUTO;
   const int G = g->n_heads / g->n_kv_heads;
-  // AUTO = the single-launch step kernel when eligible (measured >= the two-kernel path at every
-  // batch size of config 3, tools/path_sweep.py)
+  santa_status s;
   // AUTO (measured, tools/path_sweep.py -> profiles/r01_v6_path_sweep.json): the tcgen05 step kernel
   // from 1024 query heads per call with S <= 256 (batch 32: 391 vs 403 us); below that, the score
   // pass + PDL-chained sampler (batch 1: 25.0 vs 26.8 us for the mma.sync step kernel) -- the
   // sampler kernel then has every SM for the final sampling chain
-  if (path == SANTA_PATH_AUTO) path = auto_path(g, S);
+  if (path == SANTA_PATH_AUTO) path = auto_path(g, a.S);
   if (!a.events && path != SANTA_PATH_TWO_KERNEL) {
     a.tensor_core = path == SANTA_PATH_STEP_TC;
     s = dispatch<RunStep>(g->dtype, g->head_dim, G, a);
@@ -888,6 +905,17 @@ santa_status decode_common(const santa_geometry* g, const void* q, const void* K
   if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
   return last_cuda();
+}
+
+santa_status decode_common(const santa_geometry* g, const void* q, const void* K, const void* V,
+                           const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed, uint64_t offset,
+                           void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* const* events,
+                           void* stream, int path = SANTA_PATH_AUTO) {
+  DecodeArgs a;
+  const santa_status s =
+      prepare_decode(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, events, stream, path, &a);
+  if (s != SANTA_OK) return s;
+  return run_decode(a, path);
 }
 
 }  // namespace
@@ -1149,15 +1177,14 @@ santa_status santa_decode_step_host(const santa_geometry* g, const void* q_host,
                                     void* K, void* V, const int32_t* seqlens, int32_t S, int32_t mode,
                                     uint64_t seed, uint64_t offset, void* out_dev, void* out_host, void* ws,
                                     size_t ws_bytes, void* stream) {
-  santa_status s = validate_geometry(g);
-  if (s != SANTA_OK) return s;
   if (!q_host || !k_new_host || !v_new_host || !q_dev || !k_new_dev || !v_new_dev || !out_host)
     return SANTA_ERR_INVALID_ARG;
-  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
-  if ((s = validate_decode_ptrs(q_dev, K, V, seqlens, out_dev)) != SANTA_OK) return s;
-  WsLayout L;
-  if ((s = check_ws(g, S, ws, ws_bytes, &L)) != SANTA_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // the whole decode validation runs before the first copy (nothing is touched on error)
+  DecodeArgs a;
+  santa_status s = prepare_decode(g, q_dev, K, V, seqlens, S, mode, seed, offset, out_dev, nullptr, ws, ws_bytes,
+                                  nullptr, stream, SANTA_PATH_AUTO, &a);
+  if (s != SANTA_OK) return s;
+  cudaStream_t st = a.st;
   const size_t eb = elem_bytes(g->dtype), D = g->head_dim;
   const size_t qb = (size_t)g->batch * g->n_heads * D * eb, kb = (size_t)g->batch * g->n_kv_heads * D * eb;
   if (cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
@@ -1166,9 +1193,7 @@ santa_status santa_decode_step_host(const santa_geometry* g, const void* q_host,
   append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, k_new_dev, v_new_dev, kv_layout(g), seqlens,
                                                                   (int)D, (int)eb);
   if ((s = last_cuda()) != SANTA_OK) return s;
-  if ((s = decode_common(g, q_dev, K, V, seqlens, S, mode, seed, offset, out_dev, nullptr, ws, ws_bytes, nullptr,
-                         stream)) != SANTA_OK)
-    return s;
+  if ((s = run_decode(a, SANTA_PATH_AUTO)) != SANTA_OK) return s;
   if (cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SANTA_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
   return SANTA_OK;
@@ -1181,20 +1206,22 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (!qkv_host || !qkv_dev || !out_host) return SANTA_ERR_INVALID_ARG;
-  if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
   if (!aligned16(qkv_dev)) return SANTA_ERR_ALIGNMENT;
-  if ((s = validate_decode_ptrs(qkv_dev, K, V, seqlens, out_dev)) != SANTA_OK) return s;
-  WsLayout L;
-  if ((s = check_ws(g, S, ws, ws_bytes, &L)) != SANTA_OK) return s;
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const size_t eb = elem_bytes(g->dtype), D = g->head_dim;
   const size_t qb = (size_t)g->batch * g->n_heads * D * eb, kb = (size_t)g->batch * g->n_kv_heads * D * eb;
   if ((qb % 16) || (kb % 16)) return SANTA_ERR_ALIGNMENT;  // k_new / v_new sub-buffers stay 16-B aligned
-  char* dev = reinterpret_cast<char*>(qkv_dev);
   // pinned host buffers are read / written by the kernels themselves (zero copy: no copy-engine
   // round trips); pageable ones go through cudaMemcpyAsync
   const void* qkv_alias = aligned16(qkv_host) ? pinned_alias(qkv_host) : nullptr;
   void* out_alias = aligned16(out_host) ? const_cast<void*>(pinned_alias(out_host)) : nullptr;
+  // the whole decode validation runs before the first copy or launch (nothing is touched on error)
+  DecodeArgs a;
+  if ((s = prepare_decode(g, qkv_dev, K, V, seqlens, S, mode, seed, offset, out_alias ? out_alias : out_dev, nullptr,
+                          ws, ws_bytes, nullptr, stream, SANTA_PATH_AUTO, &a)) != SANTA_OK)
+    return s;
+  if (!out_alias && !out_dev) return SANTA_ERR_INVALID_ARG;
+  cudaStream_t st = a.st;
+  char* dev = reinterpret_cast<char*>(qkv_dev);
   if (qkv_alias) {
     stage_append_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(
         reinterpret_cast<const uint4*>(qkv_alias), reinterpret_cast<uint4*>(dev), K, V, kv_layout(g), seqlens, (int)D,
@@ -1205,9 +1232,7 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
                                                                     seqlens, (int)D, (int)eb);
   }
   if ((s = last_cuda()) != SANTA_OK) return s;
-  if ((s = decode_common(g, dev, K, V, seqlens, S, mode, seed, offset, out_alias ? out_alias : out_dev, nullptr, ws,
-                         ws_bytes, nullptr, stream)) != SANTA_OK)
-    return s;
+  if ((s = run_decode(a, SANTA_PATH_AUTO)) != SANTA_OK) return s;
   if (!out_alias && cudaMemcpyAsync(out_host, out_dev, qb, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return SANTA_ERR_CUDA;
   if (synchronize && cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;

@@ -22,10 +22,11 @@
 // NCCL's LL protocol, each datum is instead written together with a per-launch tag in ONE
 // single-copy-atomic store, and readers poll until the tag matches:
 //   * chunk record  [B,H,Cmax] x 16 B: two 64-bit words {m_c | tag32 << 32, l_c | tag32 << 32}
-//   * prefix stash  [B,H,Cmax,64] x 4 B: tag8 << 24 | q, q = rn(P_c[k] / l_c * (2^24 - 1)) (the
-//     in-chunk prefix as 24-bit fixed point of the chunk's mass: DESIGN.md reading #23)
+//   * prefix stash  [B,H,Cmax,32] x 8 B: tag16 << 48 | q_{2i+1} << 24 | q_{2i}, q = rn(P_c[k] / l_c *
+//     (2^24 - 1)) (the in-chunk prefix as 24-bit fixed point of the chunk's mass, two keys per
+//     word: DESIGN.md reading #23)
 //   * split partial [B,H,CS,D] x 8 B: {fp32 bits | tag32 << 32}
-// tag32 = epoch + 1, tag8 = epoch % 255 + 1, where epoch is a workspace word read by every CTA at
+// tag32 = epoch + 1, tag16 = epoch % 65535 + 1, where epoch is a workspace word read by every CTA at
 // start and bumped by the last CTA to exit (an exit ticket; the next launch is stream-ordered
 // after it).  CS > 1 splits of a head are summed in fixed split order by the split that draws
 // the last ticket (deterministic, no float atomics).  The workspace flag word is written by CTA 0
@@ -44,6 +45,8 @@ constexpr int kStepSamplers = 4;    // NSW (sampler warps per CTA)
 constexpr int kStepBarrier = 1;     // named barrier id of the sampler group
 constexpr int kStepMaxSplits = 16;  // CS limit (workspace split-partial region)
 constexpr uint32_t kQMax = 16777215u;  // 2^24 - 1
+constexpr int kStepCPT = 8;         // chunks per sampler thread in the chunk-CDF registers
+constexpr int kStepMaxChunks = kStepSamplers * 32 * kStepCPT;  // 1024 chunks = 65,536 tokens
 
 struct StepSync {
   uint32_t* epoch;            // [1]  launch epoch (tags), bumped by the last CTA to exit
@@ -63,11 +66,14 @@ constexpr int kTraceStride = 128;
 #define STEP_TRACE(slot) \
   if (sy.trace) sy.trace[(size_t)blockIdx.x * kTraceStride + (slot)] = gtimer()
 
+// Tagged-word WRITES are strong too (.relaxed.gpu): the readers poll with strong loads, and a weak
+// store racing with a strong load is a data race under the PTX memory model.  Each word is written
+// by one single-copy-atomic store, so a reader sees either the old or the new word, never a mix.
 __device__ __forceinline__ void st_v2_u64(void* p, unsigned long long a, unsigned long long b) {
-  asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 __device__ __forceinline__ void st_u64(void* p, unsigned long long a) {
-  asm volatile("st.global.u64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(a) : "memory");
 }
 // Polling loads must be STRONG (.relaxed.gpu): a weak ld (even .cg) may legally be hoisted out of
 // a spin loop by ptxas, since nothing in the loop writes memory (observed: the poll never re-read).
@@ -125,7 +131,7 @@ __device__ __forceinline__ void group_bar() { named_bar_sync(kStepBarrier, kStep
 // [KPL r, KPL r + KPL)), as warp_chunk_epilogue's L = 64 path, but publishing tagged words.
 template <int G>
 __device__ __forceinline__ void warp_chunk_epilogue_ll(const float* sS, int n_valid, uint32_t* stash_h0,
-                                                       ulonglong2* rec_h0, int Cmax, uint32_t tag32, uint32_t tag8) {
+                                                       ulonglong2* rec_h0, int Cmax, uint32_t tag32, uint32_t tag16) {
   constexpr int LPH = 32 / G;
   constexpr int KPL = 64 / LPH;  // 2, 4, 8, 16 for G = 1, 2, 4, 8
   const int lane = threadIdx.x & 31;
@@ -166,17 +172,19 @@ __device__ __forceinline__ void warp_chunk_epilogue_ll(const float* sS, int n_va
   const float excl = incl - tot;
   const float total = __shfl_sync(0xffffffffu, incl, h * LPH + LPH - 1);
   const float sc = (float)kQMax / total;  // total >= 1 (the max key contributes 2^0)
-  const uint32_t tg = tag8 << 24;
-  uint32_t q[KPL];
+  const unsigned long long tg = (unsigned long long)tag16 << 48;
+  unsigned long long q[KPL / 2];  // two 24-bit keys + the 16-bit tag per word
 #pragma unroll
-  for (int i = 0; i < KPL; ++i) q[i] = tg | min(kQMax, __float2uint_rn((v[i] + excl) * sc));
-  uint32_t* dst = stash_h0 + (size_t)h * Cmax * 64 + k0;
+  for (int i = 0; i < KPL / 2; ++i)
+    q[i] = tg | ((unsigned long long)min(kQMax, __float2uint_rn((v[2 * i + 1] + excl) * sc)) << 24) |
+           (unsigned long long)min(kQMax, __float2uint_rn((v[2 * i] + excl) * sc));
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(stash_h0 + (size_t)h * Cmax * 64 + k0);
   if constexpr (KPL >= 4) {
 #pragma unroll
-    for (int i = 0; i < KPL; i += 4)  // four independently tagged 32-bit words per 16-B store
-      *reinterpret_cast<uint4*>(dst + i) = make_uint4(q[i], q[i + 1], q[i + 2], q[i + 3]);
+    for (int i = 0; i < KPL / 2; i += 2)  // two independently tagged 64-bit words per 16-B store
+      st_v2_u64(dst + i, q[i], q[i + 1]);
   } else {
-    *reinterpret_cast<uint2*>(dst) = make_uint2(q[0], q[1]);
+    st_u64(dst, q[0]);
   }
   if (r == 0) {
     const unsigned long long t = (unsigned long long)tag32 << 32;
@@ -190,7 +198,7 @@ __device__ __forceinline__ void warp_chunk_epilogue_ll(const float* sS, int n_va
 // (reading #23).  Returns the partial sum (not yet x 1/S) in sPart[D].
 template <typename T, int D, int G, int U = 8>
 __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, int b, int h, int rank, int CS,
-                                   unsigned char* smem, int tslot, uint32_t tag32, uint32_t tag8, bool dry) {
+                                   unsigned char* smem, int tslot, uint32_t tag32, uint32_t tag16, bool dry) {
   constexpr int NT = kStepSamplers * 32, NW = kStepSamplers, NHW = NT / 16;
   const int tid = threadIdx.x - (blockDim.x - NT);  // 0..NT-1 within the group
   const int lane = tid & 31, wg = tid >> 5;
@@ -244,7 +252,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   group_bar();
 
   // ---- a3: chunk records -> fp64 chunk CDF (reading #5 clamp), values kept in registers ----
-  constexpr int kCPT = 8;                     // chunks per thread (Cmax <= 1024 on this path)
+  constexpr int kCPT = kStepCPT;              // chunks per thread (Cmax <= kStepMaxChunks, host-checked)
   const int per = (nC + NT - 1) / NT;         // <= kCPT
   const int c0 = min(tid * per, nC);
   const int nmine = min(per, nC - c0);
@@ -366,19 +374,20 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
   auto vrow = [&](int t) -> const T* {
     return p.kv.page_table ? Vb + p.kv.row(b, kvh, t, D) : vbase + (int64_t)t * D;
   };
-  const uint32_t tg = tag8 << 24;
+  const uint32_t tg16 = tag16;
+  const unsigned long long tfull = ((unsigned long long)tag16 << 48) | ((unsigned long long)kQMax << 24) | kQMax;
   for (int mw = 2 * wg; mw < Sl; mw += NHW * U) {
     const int m0 = mw + (hw & 1);
     int jj[U];
-    uint4 pv[U];
+    ulonglong2 pv[U];  // lane l: keys 4l, 4l+1 (x) and 4l+2, 4l+3 (y)
     int cc[U], nn[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int m = m0 + u * NHW;
       cc[u] = m < Sl ? sChunk[m] : -1;
       nn[u] = cc[u] >= 0 ? min(64, seqlen - cc[u] * 64) : 0;
-      pv[u] = make_uint4(tg | kQMax, tg | kQMax, tg | kQMax, tg | kQMax);
-      if (cc[u] >= 0) pv[u] = ld_strong_v4_u32(Qbase + (size_t)cc[u] * 64 + 4 * l);  // all 64 words are written
+      pv[u] = make_ulonglong2(tfull, tfull);
+      if (cc[u] >= 0) pv[u] = ld_strong_v2_u64(Qbase + (size_t)cc[u] * 64 + 4 * l);  // all 32 words are written
     }
     // validate the tags of every loaded word; re-load the stale ones (warp-uniform loop)
     {
@@ -387,10 +396,10 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
         bool bad = false;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const uint4 v = pv[u];
-          if (cc[u] >= 0 && (((v.x ^ tg) | (v.y ^ tg) | (v.z ^ tg) | (v.w ^ tg)) & 0xff000000u) != 0u) {
+          const ulonglong2 v = pv[u];
+          if (cc[u] >= 0 && ((uint32_t)(v.x >> 48) != tg16 || (uint32_t)(v.y >> 48) != tg16)) {
             bad = true;
-            pv[u] = ld_strong_v4_u32(Qbase + (size_t)cc[u] * 64 + 4 * l);
+            pv[u] = ld_strong_v2_u64(Qbase + (size_t)cc[u] * 64 + 4 * l);
           }
         }
         if (!__any_sync(0xffffffffu, bad)) break;
@@ -406,7 +415,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
       const int m = m0 + u * NHW;
       const bool on = cc[u] >= 0;
       const uint32_t tq = on ? sTq[m] : 0u;
-      const uint4 v = pv[u];
+      const ulonglong2 v = pv[u];
       const int kb = 4 * l, n = nn[u];
       // k1 = #{k < n : q[k] <= tq} = min{k : q[k] > tq}; k2 = #{k < n : q[k] < qmax} = the first key
       // reaching the chunk's full mass (used when rounding puts tq at/after it)
@@ -415,8 +424,10 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
       // word (lane j's 4 keys are 4j..4j+3) plus the crossing lane's own count of its 4 words.
       // With tq >= the full mass (rounding) the count runs to n; then the last positive-mass key,
       // the first key holding the full mass, is taken instead.
-      const uint32_t qx = kb < n ? (v.x & kQMax) : kQMax, qy = kb + 1 < n ? (v.y & kQMax) : kQMax;
-      const uint32_t qz = kb + 2 < n ? (v.z & kQMax) : kQMax, qw = kb + 3 < n ? (v.w & kQMax) : kQMax;
+      const uint32_t qx = kb < n ? ((uint32_t)v.x & kQMax) : kQMax;
+      const uint32_t qy = kb + 1 < n ? ((uint32_t)(v.x >> 24) & kQMax) : kQMax;
+      const uint32_t qz = kb + 2 < n ? ((uint32_t)v.y & kQMax) : kQMax;
+      const uint32_t qw = kb + 3 < n ? ((uint32_t)(v.y >> 24) & kQMax) : kQMax;
       const uint32_t tqe = tq < kQMax ? tq : kQMax - 1u;  // q <= tqe <=> q <= tq, except at the full mass
       const int full_lanes = __popc(__ballot_sync(0xffffffffu, qw <= tqe) & hmask);  // lanes entirely <= tq
       const int own = (qx <= tqe) + (qy <= tqe) + (qz <= tqe) + (qw <= tqe);
@@ -479,7 +490,7 @@ __device__ float* step_sample_item(const SampleParams& p, const StepSync& sy, in
 // Sampler warps are the LAST NSW warps of the CTA.
 template <typename T, int D, int G, int NSW, int U = 8>
 __device__ __forceinline__ void step_sampler_loop(const SampleParams& sp, const StepSync& sy, unsigned char* samp_smem,
-                                                  uint32_t tag32, uint32_t tag8) {
+                                                  uint32_t tag32, uint32_t tag16) {
   const int grid = gridDim.x;
   const int gtid = threadIdx.x - (blockDim.x - NSW * 32);
   __shared__ uint32_t sTicket;
@@ -490,7 +501,7 @@ __device__ __forceinline__ void step_sampler_loop(const SampleParams& sp, const 
     const int rank = it % CS, bh = it / CS;
     const int b = bh / sp.H, h = bh - b * sp.H;
     const int tslot = (sy.trace && ord < 3) ? 24 + 10 * ord : -1;
-    const float* sPart = step_sample_item<T, D, G, U>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag8, false);
+    const float* sPart = step_sample_item<T, D, G, U>(sp, sy, b, h, rank, CS, samp_smem, tslot, tag32, tag16, false);
     if (CS == 1) {
       for (int d = gtid; d < D; d += NSW * 32) store_out<T, D>(sp, (size_t)bh, d, sPart[d] * invS);
     } else {
@@ -570,7 +581,7 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
   }
   __syncthreads();
   const uint32_t epoch = sEpoch;
-  const uint32_t tag32 = epoch + 1u, tag8 = epoch % 255u + 1u;
+  const uint32_t tag32 = epoch + 1u, tag16 = epoch % 65535u + 1u;
 
   const int total = p.B * p.Hkv * p.Cmax;
   const int grid = gridDim.x;
@@ -740,7 +751,7 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
       }
       if constexpr ((kVar & 1) == 0)
         warp_chunk_epilogue_ll<G>(sS, n_valid, sy.stash + (bh0 * p.Cmax + c) * 64, sy.rec + bh0 * p.Cmax + c,
-                                  p.Cmax, tag32, tag8);
+                                  p.Cmax, tag32, tag16);
       __syncwarp();
       ++ndone;
       if (sy.trace) t_epi += gtimer() - tm1;
@@ -757,7 +768,7 @@ __global__ void __launch_bounds__(32 * (NW + 1 + NSW), 1)
     // ---------------- sampler group ----------------
     // 4 samples in flight per half-warp (tools/path_sweep.py, batch 32: S = 256 403 -> 395 us,
     // S = 512 435 -> 419 us; the tcgen05 kernel keeps 8: its S = 64 / 512 points got slower)
-    step_sampler_loop<T, D, G, NSW, 4>(sp, sy, samp_smem, tag32, tag8);
+    step_sampler_loop<T, D, G, NSW, 4>(sp, sy, samp_smem, tag32, tag16);
   }
   // ---------------- exit ticket: the last CTA out advances the epoch ----------------
   __syncthreads();

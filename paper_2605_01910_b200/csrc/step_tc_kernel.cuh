@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1)
   tc_fence_after();
   const uint32_t tmem_base = sTmem;
   const uint32_t epoch = sEpoch;
-  const uint32_t tag32 = epoch + 1u, tag8 = epoch % 255u + 1u;
+  const uint32_t tag32 = epoch + 1u, tag16 = epoch % 65535u + 1u;
 
   const int T2 = (p.Cmax + 1) / 2;           // tiles per unit
   const int total = p.B * p.Hkv * T2;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1)
           const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
           const int c = 2 * c2 + wq;
           warp_chunk_epilogue_ll<G>(sS + wq * G * 64, nv, sy.stash + (bh0 * p.Cmax + c) * 64,
-                                    sy.rec + bh0 * p.Cmax + c, p.Cmax, tag32, tag8);
+                                    sy.rec + bh0 * p.Cmax + c, p.Cmax, tag32, tag16);
         }
       }
       named_bar_sync(2 + e, 128);  // sS is rewritten by the group's next tile
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(32 * kTcWarps, 1)
   } else if (warp >= kTcSamplerWarp0) {
     // ---------------- sampler group ----------------
     setmaxnreg_inc<200>();
-    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag8);
+    step_sampler_loop<T, D, G, NSW>(sp, sy, samp_smem, tag32, tag16);
   }
   // ---------------- teardown: TMEM, then the exit ticket (the last CTA out advances the epoch) ----
   tc_fence_before();

@@ -136,3 +136,32 @@ def test_prop_and_flash_host_logic():
                                          None) == 1
     assert L.santa_decode_attention_flash(ctypes.byref(g), *a, 8, 100, 0, 0, 16, None, 256, 1 << 30, None) == 1
     assert L.santa_decode_attention_flash(ctypes.byref(g), *a, 0, 256, 0, 0, 16, None, 256, 1 << 30, None) == 3
+
+
+def test_wrappers_refuse_mismatched_cache_shapes():
+    """for a contiguous cache the row stride of K/V IS max_seqlen; the convenience
+    wrappers refuse a max_seqlen different from K.shape[2], K/V shape or dtype mismatches and a
+    malformed paged pool -- before any CUDA call (these are CPU tensors)."""
+    B, H, Hkv, n, d = 2, 8, 2, 256, 64
+    q = torch.zeros(B, H, d, dtype=torch.bfloat16)
+    K = torch.zeros(B, Hkv, n, d, dtype=torch.bfloat16)
+    V = torch.zeros_like(K)
+    sl = torch.full((B,), n, dtype=torch.int32)
+    for fn in (lambda **kw: santa.decode(q, K, V, sl, 16, **kw),
+               lambda **kw: santa.decode_prop(q, K, V, sl, 16, **kw),
+               lambda **kw: santa.decode_flash(q, K, V, sl, 16, 64, **kw),
+               lambda **kw: santa.dense(q, K, V, sl, **kw)):
+        with pytest.raises(ValueError, match="max_seqlen"):
+            fn(max_seqlen=128)                       # smaller than the row stride
+    with pytest.raises(ValueError, match="dtype"):
+        santa.decode(q, K, V.float(), sl, 16)
+    with pytest.raises(ValueError, match="shapes differ"):
+        santa.decode(q, K, V[:, :, :128], sl, 16)
+    with pytest.raises(ValueError, match="H_kv"):
+        santa.decode(q, K[:, :1], V[:, :1], sl, 16, n_kv_heads=2)
+    pool = torch.zeros(8, Hkv, 64, d, dtype=torch.bfloat16)
+    pt = torch.zeros(B, 4, dtype=torch.int64)
+    with pytest.raises(ValueError, match="page_table"):
+        santa.decode(q, pool, pool, sl, 16, page_table=pt, page_size=64)
+    with pytest.raises(ValueError, match="paged pool"):
+        santa.decode(q, pool, pool, sl, 16, page_table=pt.int(), page_size=32)

@@ -122,8 +122,11 @@ def test_bernoulli_plus_santa_index_parity():
     sc, _ = o.bernoulli_scores(si.as_bits(inp.q), si.as_bits(inp.Kt), n, nB, True, True, seed=13, offset=0)
     out_o, idx_o, det = o.santa_from_scores(sc, si.as_bits(inp.V), n, S, "stratified", 13, 0, return_details=True)
     idx_g = idx.cpu().numpy().astype(np.int64)
-    total, mism, exempt, fails = o.index_mismatch_report(det["F"], det["T"], idx_o, idx_g, tol=1e-5)
+    # the north-star exemption (reading #19) at its stated 1e-6, as for the exact score stage
+    total, mism, exempt, fails = o.index_mismatch_report(det["F"], det["T"], idx_o, idx_g, tol=1e-6)
+    print(f"config-5 index parity: {mism} mismatches of {total} samples ({mism / total:.2e}), {exempt} exempt")
     assert not fails, fails[:5]
+    assert mism <= 5e-3 * total, (mism, total)
     ref = o.out_given_idx(si.as_bits(inp.V), idx_g)
     assert np.abs(out.float().cpu().numpy() - ref).max() <= TOL["bf16"]
 

@@ -16,7 +16,7 @@ from oracle import santa_oracle as o  # noqa: E402
 
 try:
     import paper_2605_01910_b200 as santa  # noqa: E402
-    from gpu_helpers import TOL, to_cuda  # noqa: E402
+    from gpu_helpers import TOL, flash_parity, to_cuda  # noqa: E402
 except ImportError:  # library not built: the gpu tests must fail loudly, not skip
     santa = None
 
@@ -38,47 +38,6 @@ def gpu_flash(inp, S, tile_len, seed, offset=0, paged=False, head_offset=0, batc
                                       max_seqlen=max_seqlen, **kw)
     torch.cuda.synchronize()
     return out, idx
-
-
-def flash_parity(inp, out_g, idx_g, S, tile_len, seed, offset=0, head_offset=0, batch_offset=0):
-    """Returns (samples compared, index mismatches (all boundary-exempt))."""
-    q, K, V = si.as_bits(inp.q), si.as_bits(inp.K), si.as_bits(inp.V)
-    seqlens = inp.seqlens.cpu().numpy()
-    _, idx_o, det = o.santa_flash_decode(q, K, V, seqlens, S, seed, offset, B_tile=tile_len,
-                                         head_offset=head_offset, batch_offset=batch_offset, return_details=True)
-    idx_g = idx_g.cpu().numpy().astype(np.int64)
-    Vf = o.to_f64(V)
-    G = inp.q.shape[1] // V.shape[1]
-    got = out_g.float().cpu().numpy().astype(np.float64)
-    compared = mism = 0
-    for (b, h), dd in det.items():
-        n = int(seqlens[b])
-        St, T = dd["S_tile"], dd["m"].shape[0]
-        M = St * T
-        ig = idx_g[b, h]
-        assert np.all(ig[M:] == -1), (b, h)
-        ig = ig[:M]
-        io = idx_o[b, h, :M]
-        assert ig.min() >= 0 and ig.max() < n and np.all(np.diff(ig) >= 0), (b, h)
-        assert np.array_equal(np.bincount(ig // tile_len, minlength=T), np.full(T, St)), (b, h)
-        for m in np.nonzero(io != ig)[0]:
-            t, j = m // St, m % St + 1
-            lo, hi = min(io[m], ig[m]), max(io[m], ig[m])
-            u = dd["u"][t * tile_len:min((t + 1) * tile_len, n)]
-            y = dd["a0"][t] + np.cumsum(u)[lo - t * tile_len:hi - t * tile_len] * (St / dd["l"][t])
-            assert np.all(np.abs(y - j) <= 1e-5 * St + 1e-6), (b, h, m, io[m], ig[m], y - j)
-        mism += int((io != ig).sum())
-        compared += M
-        # the oracle's merge of the GPU's rows
-        Vb = Vf[b, h // G, :n]
-        O_t = np.zeros((T, Vb.shape[1]))
-        for r in ig:
-            O_t[r // tile_len] += Vb[r]
-        ref = o.flash_merge(dd["m"], dd["l"], O_t, St)
-        err = np.abs(got[b, h] - ref).max()
-        assert err <= TOL[inp.dtype], f"({b},{h}) output max-abs err {err} > {TOL[inp.dtype]}"
-    assert mism <= 5e-3 * compared, (mism, compared)
-    return compared, mism
 
 
 def test_max_samples_and_invalid_tiles():
@@ -195,7 +154,7 @@ def test_flash_unbiased_gpu():
 def test_prop_and_flash_long_context(n):
     """Long contexts: 4688 / 9375 score chunks per sequence; beyond 512k tokens the chunk (and so
     prop's tile) is 128 keys.  Both estimators against the oracle on one GQA group."""
-    from test_gpu_prop import prop_parity
+    from gpu_helpers import prop_parity
     inp = to_cuda(si.make_decode_inputs(1, 4, 1, 128, n, dtype="bf16", seed=40, workload="temp4"))
     geo = santa.make_geometry(inp.q, 1, n)
     tile = santa.santa_prop_tile_len(geo)

@@ -142,6 +142,53 @@ def test_invalid_arguments_launch_nothing():
     assert torch.all(out == 3.0)
 
 
+@pytest.mark.parametrize("path", ["step", "step_tc"])
+def test_forced_step_paths_refuse_long_contexts(path):
+    """the step kernels' sampler keeps <= 1024 chunk statistics per head in
+    registers, so a forced step path on max_seqlen > 65,536 must return SANTA_ERR_UNSUPPORTED and
+    launch nothing (AUTO takes the two-kernel path there)."""
+    n = 65536 + 64
+    inp = to_cuda(si.make_decode_inputs(1, 8, 2, 128, n, dtype="bf16", seed=7))
+    geo = santa.make_geometry(inp.q, 2, n)
+    ws = santa.workspace(geo, 64)
+    out = torch.full_like(inp.q, 3.0)
+    with pytest.raises(santa.SantaError) as e:
+        santa.santa_decode_attention_path(geo, inp.q, inp.K, inp.V, inp.seqlens, 64, 1, 1, 0, out, None, ws, path)
+    assert e.value.status == 5
+    torch.cuda.synchronize()
+    assert torch.all(out == 3.0)
+    assert santa.santa_auto_path(geo, 64) == "two_kernel"
+    got, idx = gpu_decode(inp, 64, "stratified", seed=1)   # AUTO on the same geometry works
+    check_parity(inp, got, idx, 64, "stratified", seed=1)
+
+
+def test_host_step_apis_validate_before_touching_the_cache():
+    """santa_decode_step_host(_packed) run every decode check BEFORE the first copy or
+    launch, so an invalid call (S too large, bad mode) leaves the K/V cache and outputs untouched."""
+    B, H, Hkv, d = 1, 8, 2, 128
+    inp = to_cuda(si.make_decode_inputs(B, H, Hkv, d, 300, dtype="bf16", seed=7))
+    geo = santa.make_geometry(inp.q, Hkv, 300)
+    ws = santa.workspace(geo, 8)
+    K0, V0 = inp.K.clone(), inp.V.clone()
+    qkv = torch.randn(B * H * d + 2 * B * Hkv * d).to(torch.bfloat16).pin_memory()
+    out_h = torch.full((B * H * d,), 3.0, dtype=torch.bfloat16).pin_memory()
+    dev = torch.empty(B * H * d + 2 * B * Hkv * d, dtype=torch.bfloat16, device="cuda")
+    od = torch.full_like(inp.q, 3.0)
+    for S, mode, status in [(5000, 1, 5), (8, 7, 1), (0, 1, 3)]:
+        with pytest.raises(santa.SantaError) as e:
+            santa.santa_decode_step_host_packed(geo, qkv, dev, inp.K, inp.V, inp.seqlens, S, mode, 1, 0, od, out_h, ws)
+        assert e.value.status == status
+        qh, kh, vh = (torch.randn(B, h_, d).to(torch.bfloat16).pin_memory() for h_ in (H, Hkv, Hkv))
+        with pytest.raises(santa.SantaError) as e:
+            santa.santa_decode_step_host(geo, qh, kh, vh, torch.empty_like(inp.q), torch.empty(B, Hkv, d, dtype=torch.bfloat16, device="cuda"),
+                                         torch.empty(B, Hkv, d, dtype=torch.bfloat16, device="cuda"), inp.K, inp.V,
+                                         inp.seqlens, S, mode, 1, 0, od, out_h, ws)
+        assert e.value.status == status
+    torch.cuda.synchronize()
+    assert torch.equal(inp.K, K0) and torch.equal(inp.V, V0)
+    assert torch.all(od == 3.0) and torch.all(out_h == 3.0)
+
+
 def test_determinism_bitwise():
     inp = to_cuda(si.make_decode_inputs(2, 32, 8, 128, [3000, 2500], dtype="bf16", seed=8))
     a = gpu_decode(inp, 256, "stratified", seed=3)

@@ -15,7 +15,7 @@ from oracle import santa_oracle as o  # noqa: E402
 
 try:
     import paper_2605_01910_b200 as santa  # noqa: E402
-    from gpu_helpers import TOL, to_cuda  # noqa: E402
+    from gpu_helpers import TOL, lr_valid, prop_parity, to_cuda  # noqa: E402
 except ImportError:  # library not built: the gpu tests must fail loudly, not skip
     santa = None
 
@@ -37,63 +37,6 @@ def gpu_prop(inp, S, seed, offset=0, paged=False, head_offset=0, batch_offset=0,
                                      return_idx=True, head_offset=head_offset, batch_offset=batch_offset)
     torch.cuda.synchronize()
     return out, idx
-
-
-def lr_valid(Sg, q, S, tol):
-    """Sg is a largest-remainder allocation of quotas within tol of q: sum = S, every S_t within
-    1 + tol of q_t, and no tile rounded down keeps a larger remainder than a tile rounded up."""
-    if int(Sg.sum()) != S or np.any(np.abs(Sg - q) >= 1 + tol):
-        return False
-    up = Sg > q
-    down_rem = (q - Sg)[~up]
-    up_rem = (1.0 - (Sg - q))[up]
-    if down_rem.size == 0 or up_rem.size == 0:
-        return True
-    return down_rem.max() <= up_rem.min() + 2 * tol
-
-
-def prop_parity(inp, out_g, idx_g, S, seed, offset=0, head_offset=0, batch_offset=0, B_tile=64,
-                max_budget_mismatch=0.25):
-    """Returns (heads, heads with different budgets, samples compared, index mismatches, exempt)."""
-    q, K, V = si.as_bits(inp.q), si.as_bits(inp.K), si.as_bits(inp.V)
-    seqlens = inp.seqlens.cpu().numpy()
-    _, idx_o, det = o.santa_prop_decode(q, K, V, seqlens, S, seed, offset, B_tile=B_tile,
-                                        head_offset=head_offset, batch_offset=batch_offset, return_details=True)
-    idx_g = idx_g.cpu().numpy().astype(np.int64)
-    tol_q = 2e-5 * S + 1e-9
-    heads = budget_diff = compared = mism = exempt = 0
-    for (b, h), dd in det.items():
-        heads += 1
-        n = int(seqlens[b])
-        ig = idx_g[b, h]
-        assert ig.min() >= 0 and ig.max() < n and np.all(np.diff(ig) >= 0), (b, h)
-        T = dd["St"].shape[0]
-        Sg = np.bincount(ig // B_tile, minlength=T)
-        assert Sg.shape[0] == T
-        if not np.array_equal(Sg, dd["St"]):
-            budget_diff += 1
-            assert lr_valid(Sg, dd["q"], S, tol_q), (b, h, np.nonzero(Sg != dd["St"]))
-            continue
-        # equal budgets: the same tile-major sample list up to count boundaries at rounding distance
-        io = idx_o[b, h]
-        u, a0, St = dd["u"], dd["a0"], dd["St"]
-        for m in np.nonzero(io != ig)[0]:
-            t = io[m] // B_tile
-            j = m - int(St[:t].sum()) + 1
-            lo, hi = min(io[m], ig[m]), max(io[m], ig[m])
-            Ut = np.cumsum(u[t * B_tile:min((t + 1) * B_tile, n)]) * (St[t] / dd["l"][t])
-            y = a0[t] + Ut[lo - t * B_tile:hi - t * B_tile]
-            tol_c = 1e-5 * St[t] + 1e-6
-            assert np.all(np.abs(y - j) <= tol_c), (b, h, m, io[m], ig[m], y - j)
-            exempt += 1
-        mism += int((io != ig).sum())
-        compared += S
-    assert budget_diff <= max_budget_mismatch * heads, (budget_diff, heads)
-    ref = o.out_given_idx(V, idx_g)
-    got = out_g.float().cpu().numpy().astype(np.float64)
-    err = np.abs(got - ref).max()
-    assert err <= TOL[inp.dtype], f"output max-abs err {err} > {TOL[inp.dtype]}"
-    return heads, budget_diff, compared, mism, exempt
 
 
 def test_tile_len_is_the_chunk_length():
@@ -225,4 +168,4 @@ def test_prop_exact_ties_go_to_lower_tiles(T, S):
     want = np.array([base + 1] * R + [base] * (T - R))
     for h in range(2):
         assert np.array_equal(np.bincount(idx[0, h].cpu().numpy() // 64, minlength=T), want)
-    prop_parity(inp, out, idx, S, 7, max_budget_mismatch=0.0)
+    prop_parity(inp, out, idx, S, 7)
