@@ -66,10 +66,12 @@ def check_parity(inp, out_gpu, idx_gpu, S, mode, seed, offset=0, head_offset=0, 
 
 # ---- S^2ANTA-prop / -flash row parity (readings #25, #26) --------------------------------------
 # The tile estimators decide rows by comparing the tile's uniform a0 with count boundaries:
-# row j of tile t is min{n : a0 + U_n S_t / l_t >= j}.  The north-star rule ("a uniform within
-# 1e-6 of a CDF boundary") carried to the tile: a GPU/oracle row mismatch is exempt iff every
-# crossed boundary y = a0 + U_n S_t / l_t lies within ROW_TOL of the integer j -- the uniform a0
-# within 1e-6 of the boundary j - U_n S_t / l_t.
+# row j of tile t is min{n : a0 + U_n S_t / l_t >= j}, i.e. the in-tile threshold
+# tau_j = (j - a0) / S_t against the tile CDF U_n / l_t.  The north-star rule ("a uniform within
+# 1e-6 of a CDF boundary") carried to the tile, in the same units as the exact path's rule (CDF
+# units, where T_m = (m + u_m) / S is compared with F): a GPU/oracle row mismatch is exempt iff
+# every crossed tile-CDF boundary U_n / l_t lies within ROW_TOL of tau_j, i.e. |y - j| <= ROW_TOL * S_t
+# with y = a0 + U_n S_t / l_t (reading #25; "1e-6 in tile-CDF units").
 ROW_TOL = 1e-6
 
 
@@ -89,7 +91,7 @@ def lr_valid(Sg, q, S, tol):
 def _row_boundaries_near(dd, t, B_tile, n, St_t, lo, hi, j):
     u = dd["u"][t * B_tile:min((t + 1) * B_tile, n)]
     y = dd["a0"][t] + np.cumsum(u)[lo - t * B_tile:hi - t * B_tile] * (St_t / dd["l"][t])
-    return bool(np.all(np.abs(y - j) <= ROW_TOL)), y - j
+    return bool(np.all(np.abs(y - j) <= ROW_TOL * St_t)), (y - j) / St_t
 
 
 def prop_parity(inp, out_g, idx_g, S, seed, offset=0, head_offset=0, batch_offset=0, B_tile=64):
