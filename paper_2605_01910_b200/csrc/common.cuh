@@ -20,11 +20,48 @@ __device__ __forceinline__ void pdl_wait_primary() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// globaltimer (ns): tools-only phase traces
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- exp2 (MUFU) -----------------------------------------------------------------------
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x in fp64 for x < 1023 (chunk weights 2^(m_c - m*)), without the library exp2:
+// x = n + f, n = rint(x), f in [-1/2, 1/2]; e^(f ln2) by its Taylor series to degree 13
+// (truncation < 5e-18 relative) and an exact scale by 2^n.  Returns 0 below 2^-1022.
+__device__ __forceinline__ double exp2_fast(double x) {
+  if (!(x > -1022.0)) return 0.0;
+  const double n = rint(x);
+  const double g = (x - n) * 0.69314718055994530942;
+  double r = 1.0 / 6227020800.0;  // 1/13!
+  r = fma(r, g, 1.0 / 479001600.0);
+  r = fma(r, g, 1.0 / 39916800.0);
+  r = fma(r, g, 1.0 / 3628800.0);
+  r = fma(r, g, 1.0 / 362880.0);
+  r = fma(r, g, 1.0 / 40320.0);
+  r = fma(r, g, 1.0 / 5040.0);
+  r = fma(r, g, 1.0 / 720.0);
+  r = fma(r, g, 1.0 / 120.0);
+  r = fma(r, g, 1.0 / 24.0);
+  r = fma(r, g, 1.0 / 6.0);
+  r = fma(r, g, 0.5);
+  r = fma(r, g, 1.0);
+  r = fma(r, g, 1.0);
+  return r * __longlong_as_double((long long)((int)n + 1023) << 52);
 }
 
 // ---- streaming 128-bit global loads (read once: do not allocate in L1) -----------------

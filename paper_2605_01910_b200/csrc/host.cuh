@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -20,6 +21,7 @@
 #include "philox.cuh"
 #include "prop_kernels.cuh"
 #include "sample_kernels.cuh"
+#include "sample_fast.cuh"
 #include "score_kernels.cuh"
 #include "step_kernel.cuh"
 #include "step_tc_kernel.cuh"

@@ -41,6 +41,39 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
 template <typename T, int D, int G>
 santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   SampleParams p = make_sample_params(a);
+  if (p.L == 64 && a.stats_all == nullptr) {  // the low-latency sampler (sample_fast.cuh)
+    const int heads = a.g->batch * a.g->n_heads;
+    // CTAs per head: up to a 4-CTA cluster while the grid stays one wave (config 2: 32 heads x 4;
+    // tools/tail_sweep.py: CS = 1 / 2 / 4 -> 26.8 / 24.6 / 22.6 us per step), >= 8 strata per CTA
+    int CS = 1;
+    while (CS < 4 && heads * CS * 2 <= num_sms() && CS * 2 * 8 <= a.S) CS *= 2;
+    p.cluster = CS;
+    const size_t smem = sample_fast_smem_bytes(p.Cmax, D, CS);
+    if (ensure_smem(sample_fast_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+    if (a.events) cudaEventRecord(a.events[1], a.st);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.g->n_heads * CS, a.g->batch);
+    cfg.blockDim = dim3(kFastThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = a.st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CS;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+    if (a.events == nullptr) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    if (cudaLaunchKernelEx(&cfg, sample_fast_kernel<T, D, G>, p) != cudaSuccess) return SANTA_ERR_CUDA;
+    if (a.events) cudaEventRecord(a.events[2], a.st);
+    return SANTA_OK;
+  }
   // CTAs per head: a thread-block cluster of CS CTAs splits the S strata (more SMs on the
   // latency-bound search/gather), partials summed through DSMEM.  Aim at >= ~2 CTAs per SM.
   int CS = 1;

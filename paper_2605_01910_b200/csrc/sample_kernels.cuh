@@ -57,11 +57,6 @@ struct SampleParams {
   unsigned long long* trace;    // NULL in the library; tools/microbench_sample.cu phase timing
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 #define SANTA_TRACE(i)                                                   \
   if (p.trace && threadIdx.x == 0 && rank == 0)                          \
   p.trace[((size_t)b * p.H + h) * 16 + (i)] = gtimer()

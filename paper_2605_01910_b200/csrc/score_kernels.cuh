@@ -286,6 +286,9 @@ __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const
     if (blockIdx.x == 0 && p.flags) *p.flags = 0u;
   }
   __syncthreads();
+#ifdef SANTA_SCORE_EARLY_TRIGGER
+  pdl_launch_dependents();
+#endif
 
   // chunks interleaved over the grid (7 % faster streaming than contiguous CTA ranges,
   // tools/microbench_b2b.cu): warp j of CTA i takes w = i + (j + NW t) * grid, t = 0, 1, ...

@@ -100,30 +100,6 @@ __device__ __forceinline__ bool rec_valid(const ulonglong2& r, uint32_t tag32) {
 }
 __device__ __forceinline__ bool poll_expired(unsigned long long t0) { return gtimer() - t0 > 500000000ull; }
 
-// 2^x in fp64 for x < 1023 (chunk weights 2^(m_c - m*)), without the library exp2:
-// x = n + f, n = rint(x), f in [-1/2, 1/2]; e^(f ln2) by its Taylor series to degree 13
-// (truncation < 5e-18 relative) and an exact scale by 2^n.  Returns 0 below 2^-1022.
-__device__ __forceinline__ double exp2_fast(double x) {
-  if (!(x > -1022.0)) return 0.0;
-  const double n = rint(x);
-  const double g = (x - n) * 0.69314718055994530942;
-  double r = 1.0 / 6227020800.0;  // 1/13!
-  r = fma(r, g, 1.0 / 479001600.0);
-  r = fma(r, g, 1.0 / 39916800.0);
-  r = fma(r, g, 1.0 / 3628800.0);
-  r = fma(r, g, 1.0 / 362880.0);
-  r = fma(r, g, 1.0 / 40320.0);
-  r = fma(r, g, 1.0 / 5040.0);
-  r = fma(r, g, 1.0 / 720.0);
-  r = fma(r, g, 1.0 / 120.0);
-  r = fma(r, g, 1.0 / 24.0);
-  r = fma(r, g, 1.0 / 6.0);
-  r = fma(r, g, 0.5);
-  r = fma(r, g, 1.0);
-  r = fma(r, g, 1.0);
-  return r * __longlong_as_double((long long)((int)n + 1023) << 52);
-}
-
 __device__ __forceinline__ void group_bar() { named_bar_sync(kStepBarrier, kStepSamplers * 32); }
 
 // ---------------------------------------------------------------------------------------
