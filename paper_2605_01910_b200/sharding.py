@@ -121,29 +121,42 @@ class CudaBackend:
         return partial, idx
 
 
+def shard_ranges(seqlens, rank: int, world: int, device=None):
+    """This rank's contiguous token range of every sequence: (token_offset [B] int32, shard_len [B]
+    int32), rank r holding [r*n//R, (r+1)*n//R).  Host logic; computed once per sequence-length
+    change (a decode loop reuses it across steps -- no device sync on the step path)."""
+    lens = [int(s) for s in (seqlens.tolist() if torch.is_tensor(seqlens) else seqlens)]
+    lo = torch.tensor([rank * s // world for s in lens], dtype=torch.int32)
+    hi = torch.tensor([(rank + 1) * s // world for s in lens], dtype=torch.int32)
+    return lo.to(device) if device is not None else lo, (hi - lo).to(device) if device is not None else hi - lo
+
+
 def seqshard_decode(q: torch.Tensor, K_shard: torch.Tensor, V_shard: torch.Tensor, seqlens: torch.Tensor,
                     S: int, mode: str, seed: int, offset: int = 0, backend=None, group=None,
-                    return_idx: bool = False):
+                    return_idx: bool = False, ranges=None):
     """Sequence-sharded S^2ANTA decode step (config 4).  Every rank passes its own contiguous
     K/V shard [B, H_kv, n_local, d] and the FULL q [B, H, d] and seqlens [B] (global lengths).
+    ``ranges``: this rank's (token_offset, shard_len) from shard_ranges(), precomputed by a decode
+    loop (else derived from seqlens here, with a device-to-host read).
     Returns the summed output [B, H, d] fp32 on every rank (and this rank's global indices, -1
     for strata owned by other ranks, if return_idx)."""
     backend = backend or CudaBackend()
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    B = q.shape[0]
-    # this rank's token range of every sequence
     n_loc = K_shard.shape[2]
-    lo = torch.tensor([rank * int(s) // world for s in seqlens.tolist()], dtype=torch.int32)
-    hi = torch.tensor([(rank + 1) * int(s) // world for s in seqlens.tolist()], dtype=torch.int32)
-    shard_len = (hi - lo).to(q.device)
-    if int((hi - lo).max()) > n_loc:
-        raise ValueError("K_shard too short for this rank's token range")
+    if ranges is None:
+        ranges = shard_ranges(seqlens, rank, world, q.device)
+        if int(ranges[1].max()) > n_loc:
+            raise ValueError("K_shard too short for this rank's token range")
+    lo, shard_len = ranges
     stats = backend.stats(q, K_shard, shard_len, K_shard.shape[1], S)           # [B, H, 2] fp64
-    gathered = [torch.empty_like(stats) for _ in range(world)]
-    dist.all_gather(gathered, stats, group=group)                               # the exchange step
-    stats_all = torch.stack(gathered, 0)                                        # [R, B, H, 2]
-    partial, idx = backend.sample_gather(stats_all, rank, world, lo.to(q.device), V_shard, shard_len, S, mode, seed,
+    stats_all = torch.empty((world,) + tuple(stats.shape), dtype=stats.dtype, device=stats.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(stats_all, stats, group=group)              # the exchange step
+    else:
+        dist.all_gather(list(stats_all.unbind(0)), stats, group=group)
+    # stats_all: [R, B, H, 2]
+    partial, idx = backend.sample_gather(stats_all, rank, world, lo, V_shard, shard_len, S, mode, seed,
                                          offset, return_idx=return_idx)
     dist.all_reduce(partial, op=dist.ReduceOp.SUM, group=group)                 # sum of partial outputs
     return (partial, idx) if return_idx else partial
