@@ -6,11 +6,15 @@ Default (N=1): BASELINE config 2 -- Llama-3.1-8B GQA decode (H=32, H_kv=8, d=128
 32k context, batch 1, S=256 stratified, synthetic W1 (i.i.d. Gaussian) inputs.  Under
 torchrun with N ranks every rank runs its own config-2 problem with global batch id = rank
 (batch x kv-head sharding, no data-path collective -> weak scaling); NCCL is used only for
-the barrier and the max-over-ranks of the device times.
+the barrier and the max-over-ranks of the device times.  Extra legs at N > 1: config 3 as stated
+(32 sequences sharded over the N GPUs, strong scaling) and config 4 (one 512k sequence sharded
+over the N GPUs, sharding.seqshard_decode with its NCCL all-gather and all-reduce timed inside).
 
-Timing: W untimed warm-up steps; then K timed steps, each bracketed by CUDA events on the
-launching stream; the L2 (126 MB) is flushed by writing a 512 MiB buffer before every timed
-step, outside the events.  The whole timed loop is bracketed by barrier + synchronize.
+Timing (headline): W untimed warm-up steps, then K back-to-back steps bracketed by barrier +
+synchronize and CUDA events on the launching stream; the steps rotate over >= 4 distinct KV caches
+(512 MiB, > 4x the 126 MB L2), so every step streams its K from HBM -- the "inputs larger than L2"
+option (no flush between the timed steps).  isolated_latency_us is the other protocol: one call
+between CUDA events after a 512 MiB L2-flush write (the paper's).
 
 value = algorithmic bytes of all ranks / max-over-ranks mean step time, where algorithmic
 bytes = all K bytes + UNIQUE sampled V rows (union over the GQA group) + q + out
@@ -58,6 +62,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0x5A17A)
     ap.add_argument("--no-baselines", action="store_true", help="skip the FlashInfer / FA-2 / SDPA context timings")
     ap.add_argument("--no-config3", action="store_true", help="skip the BASELINE config-3 (batch 32) S sweep")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo + --share-gpu: exercise the multi-rank legs "
+                         "on one GPU; never a bench number)")
+    ap.add_argument("--share-gpu", action="store_true", help="every rank on cuda:0 (test mode, with gloo)")
     return ap.parse_args()
 
 
@@ -181,32 +189,65 @@ def run_reference(args, rank, world):
         "dtype": "f64", "data": "synthetic (seeded torch.randn, W1 Gaussian)",
         "config": {"workload": WORKLOAD, "sample": sample, "S": args.S, "mode": args.mode},
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "threads": {"python_loop": 1, "blas": cores},
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(inp_cpu, args, bytes_per_step):
-    """The oracle as it stands timed on this host on the full config-2 step, ~10 s budget."""
+    """The oracle as it stands (fp64 numpy; a Python loop over (b, h) whose only multi-threaded
+    step is the BLAS mat-vec of the scores) timed on this host on the full config-2 step: once with
+    BLAS limited to one thread and once with all cores (~5 s each), plus BASELINE config 1 (one
+    head, 1024 keys, d = 64, fp32, S = 16 systematic) in seconds."""
     import numpy as np
-    from threadpoolctl import threadpool_info
+    from threadpoolctl import threadpool_info, threadpool_limits
 
     import santa_inputs as si
     from oracle import santa_oracle as o
 
     q, K, V = si.as_bits(inp_cpu.q), si.as_bits(inp_cpu.K), si.as_bits(inp_cpu.V)
     sl = inp_cpu.seqlens.cpu().numpy()
-    times = []
-    t_start = time.perf_counter()
-    while time.perf_counter() - t_start < 10.0 or len(times) < 2:
+
+    def run(budget):
+        times = []
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < budget or len(times) < 2:
+            t0 = time.perf_counter()
+            o.santa_decode(q, K, V, sl, args.S, args.mode, args.seed, len(times))
+            times.append(time.perf_counter() - t0)
+        return float(np.median(times)), len(times), time.perf_counter() - t_start
+
+    with threadpool_limits(limits=1):
+        t1, n1, w1 = run(5.0)
+    t_all, n_all, w_all = run(5.0)
+    blas = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
+    c1 = si.make_decode_inputs(1, 1, 1, 64, 1024, dtype="f32", seed=1)
+    c1t = []
+    for i in range(7):
         t0 = time.perf_counter()
-        o.santa_decode(q, K, V, sl, args.S, args.mode, args.seed, len(times))
-        times.append(time.perf_counter() - t0)
-    t = float(np.median(times))
-    cores = max([x.get("num_threads", 1) for x in threadpool_info()] + [1])
-    return {"value": round(bytes_per_step / t / 1e9, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"full config-2 step (batch {inp_cpu.q.shape[0]}), {len(times)} steps in "
-                      f"{time.perf_counter() - t_start:.1f} s, median {t * 1e3:.0f} ms/step"}
+        o.santa_decode(si.as_bits(c1.q), si.as_bits(c1.K), si.as_bits(c1.V), [1024], 16, "systematic", args.seed, i)
+        c1t.append(time.perf_counter() - t0)
+    return {"value": round(bytes_per_step / t_all / 1e9, 4), "unit": "GB/s", "cores": blas, "kind": "oracle",
+            "sample": f"full config-2 step (batch {inp_cpu.q.shape[0]}), {n_all} steps in {w_all:.1f} s, "
+                      f"median {t_all * 1e3:.0f} ms/step",
+            "threads": {"python_loop": 1, "blas": blas}, "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+            "single_thread": {"value": round(bytes_per_step / t1 / 1e9, 4), "unit": "GB/s",
+                              "ms_per_step": round(t1 * 1e3, 1), "steps": n1},
+            "all_cores": {"value": round(bytes_per_step / t_all / 1e9, 4), "unit": "GB/s",
+                          "ms_per_step": round(t_all * 1e3, 1), "steps": n_all},
+            "config1_seconds": round(float(np.median(c1t)), 5),
+            "language": "numpy fp64 (the oracle as committed, not the C++ program SURVEY 8(c) sketched)"}
 
 
 def library_baselines(probs, NR, timed_loop, args):
@@ -383,6 +424,113 @@ def config5(args, dev, stream, timed_loop, peak):
                     "bytes = selected K^T feature rows + unique V rows + q/out"}
 
 
+def config3_strong(args, dev, stream, timed_loop, max_over_ranks, peak, world, rank):
+    """BASELINE config 3 as stated -- 32 sequences of 32k SHARDED over the N GPUs by (batch, kv-head)
+    units (sharding.plan_units: contiguous slabs, global Philox ids, no collective): each rank holds
+    and decodes only its slabs; step time = max over ranks; GB/s = all 32 sequences' algorithmic
+    bytes / that time (strong scaling: total work fixed)."""
+    import torch
+
+    import paper_2605_01910_b200 as santa
+    from paper_2605_01910_b200 import sharding
+    import santa_inputs as si
+
+    B, H, Hkv, d, n = 32, 32, 8, 128, args.seqlen
+    G = H // Hkv
+    slabs = sharding.plan_units(B, Hkv, world)[rank]
+    parts = []
+    for sl in slabs:
+        nb, nk = sl.b1 - sl.b0, sl.k1 - sl.k0
+        inp = si.make_decode_inputs(nb, nk * G, nk, d, n, dtype="bf16", workload=args.workload,
+                                    seed=7700 + sl.b0 * Hkv + sl.k0, device=str(dev))
+        geo = santa.make_geometry(inp.q, nk, n, batch_offset=sl.b0, head_offset=sl.k0 * G)
+        parts.append((inp, geo, torch.empty_like(inp.q)))
+    steps = max(3, min(args.steps, 10))
+    rows = {}
+    for S in (64, 128, 256, 512):
+        wss = [santa.workspace(geo, S, dev) for _, geo, _ in parts]
+
+        def fn(i, S=S, wss=wss):
+            for (inp, geo, out), ws in zip(parts, wss):
+                santa.santa_decode_attention(geo, inp.q, inp.K, inp.V, inp.seqlens, S, args.mode, args.seed, i, out,
+                                             None, ws, stream)
+        for i in range(3):
+            fn(i)
+        t = max_over_ranks(timed_loop(fn, steps))
+        # unique V rows are counted on rank-local slabs and summed over ranks (bytes of the whole job)
+        U = 0
+        for (inp, geo, out), ws in zip(parts, wss):
+            idx = torch.empty((inp.q.shape[0], inp.q.shape[1], S), dtype=torch.int32, device=dev)
+            santa.santa_decode_attention(geo, inp.q, inp.K, inp.V, inp.seqlens, S, args.mode, args.seed, 0, out, idx,
+                                         ws, stream)
+            U += unique_rows_gpu(idx, geo.n_kv_heads)
+        U = sum_over_ranks(float(U), dev, world)
+        byt = B * Hkv * n * d * 2 + U * d * 2 + 2 * B * H * d * 2
+        rows[str(S)] = {"us": round(t * 1e3, 2), "GBps": round(byt / (t * 1e-3) / 1e9, 1),
+                        "per_gpu_frac_of_peak": round(byt / world / (t * 1e-3) / 1e9 / peak, 4)}
+        del wss
+    rows["note"] = (f"32 sequences x 32k sharded over {world} GPU(s) by (batch, kv-head) units "
+                    f"({sum(s.units for s in slabs)} units on rank {rank}); max over ranks; strong scaling")
+    del parts
+    torch.cuda.empty_cache()
+    return rows
+
+
+def sum_over_ranks(x, dev, world):
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return x
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def config4_seqshard(args, dev, stream, timed_loop, max_over_ranks, peak, world, rank):
+    """BASELINE config 4 on N GPUs: one 512k-token sequence, S = 1024 stratified by shard mass, each
+    rank holding the contiguous 512k / N tokens of every kv head; sharding.seqshard_decode with the
+    CUDA backend -- phase 1 (score pass + shard (m_r, L_r)), the all-gather of the [1, 32, 2] fp64
+    stats over the process group, phase 2 (global shard CDF, own strata, local gather), the
+    all-reduce of the [1, 32, 128] fp32 partial outputs -- timed end to end with both collectives
+    inside the events (max over ranks), and the two kernel phases alone."""
+    import torch
+
+    from paper_2605_01910_b200 import sharding
+    import santa_inputs as si
+
+    H, Hkv, d, S, n = 32, 8, 128, 1024, 524288
+    seqlens = torch.tensor([n], dtype=torch.int32, device=dev)
+    ranges = sharding.shard_ranges([n], rank, world, dev)
+    nloc = int(ranges[1][0].item())
+    loc = si.make_decode_inputs(1, H, Hkv, d, nloc, dtype="bf16", workload=args.workload, seed=900 + rank,
+                                device=str(dev))
+    q = si.make_decode_inputs(1, H, Hkv, d, 16, dtype="bf16", seed=899, device=str(dev)).q  # same q everywhere
+    be = sharding.CudaBackend()
+    steps = max(3, min(args.steps, 20))
+
+    def full(i):
+        sharding.seqshard_decode(q, loc.K, loc.V, seqlens, S, args.mode, args.seed, i, backend=be, ranges=ranges)
+    for i in range(3):
+        full(i)
+    t = max_over_ranks(timed_loop(full, steps))
+    st = be.stats(q, loc.K, ranges[1], Hkv, S)
+    stats_all = st.unsqueeze(0).repeat(world, 1, 1, 1).contiguous()
+    t1 = max_over_ranks(timed_loop(lambda i: be.stats(q, loc.K, ranges[1], Hkv, S), steps))
+    t2 = max_over_ranks(timed_loop(lambda i: be.sample_gather(stats_all, rank, world, ranges[0], loc.V, ranges[1], S,
+                                                              args.mode, args.seed, i), steps))
+    kb = Hkv * n * d * 2
+    out = {"R": world, "us": round(t * 1e3, 2), "GBps": round(kb / (t * 1e-3) / 1e9, 1),
+           "per_gpu_frac_of_peak": round(kb / world / (t * 1e-3) / 1e9 / peak, 4),
+           "kernel_only_us": {"phase1": round(t1 * 1e3, 2), "phase2": round(t2 * 1e3, 2)},
+           "collectives_us": round(max(0.0, t - t1 - t2) * 1e3, 2),
+           "note": ("seqshard_decode end to end (score pass, all_gather of (m_r, L_r), sampler + gather, "
+                    f"all_reduce of the partials) over {args.dist_backend}; GB/s counts the K bytes of the "
+                    "whole 512k sequence")}
+    del loc, be
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -402,10 +550,15 @@ def main():
     import paper_2605_01910_b200 as santa
     import santa_inputs as si
 
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", 0 if args.share_gpu else local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # comm_nranks etc. on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     B, H, Hkv, d, n = args.batch, 32, 8, 128, args.seqlen
     G = H // Hkv
@@ -711,6 +864,15 @@ def main():
         if world == 1:
             res["config4_per_rank"] = config4(args, dev, stream, timed_loop, peak)
             res["config5"] = config5(args, dev, stream, timed_loop, peak)
+        else:
+            res["config3_strong"] = config3_strong(args, dev, stream, timed_loop, max_over_ranks, peak, world, rank)
+            res["config4_seqshard"] = config4_seqshard(args, dev, stream, timed_loop, max_over_ranks, peak, world,
+                                                       rank)
+    if world > 1:
+        res["distributed"] = {"backend": args.dist_backend, "world": world,
+                              "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))
+                              if args.dist_backend == "nccl" else None,
+                              "nccl_debug": os.environ.get("NCCL_DEBUG")}
     if not args.no_extras and not args.no_baselines and rank == 0 and args.batch == 1 and not args.page_size:
         res["library_baselines"] = library_baselines(probs, NR, timed_loop, args)
         d = res["library_baselines"]
