@@ -554,8 +554,8 @@ def main():
     torch.cuda.set_device(dev)
     if world > 1:
         if args.dist_backend == "nccl":
-            os.environ.setdefault("NCCL_DEBUG", "INFO")          # comm_nranks etc. on stderr
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ["NCCL_DEBUG"] = "INFO"            # comm_nranks / nvls / channels on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")

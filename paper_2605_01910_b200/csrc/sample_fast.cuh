@@ -194,7 +194,7 @@ __device__ __forceinline__ void fast_block_chunks(const float2* cs, int c0, int 
   float2 st[R];
   float mloc = -INFINITY;
   if constexpr (PER == 2) {
-    if (c0 + 2 <= c1 && (c0 & 1) == 0) {
+    if (c0 + 2 <= c1 && (reinterpret_cast<uintptr_t>(cs + c0) & 15u) == 0) {  // 16-B aligned pair
       const float4 v = __ldcg(reinterpret_cast<const float4*>(cs + c0));
       st[0] = make_float2(v.x, v.y);
       st[1] = make_float2(v.z, v.w);

@@ -330,3 +330,11 @@ def test_report_mismatch_rates(capsys):
     with capsys.disabled():
         for r in REPORT:
             print("index parity", r)
+
+
+def test_odd_chunk_strides_and_unaligned_stats_rows():
+    """Chunk-stat rows of odd length (Cmax odd: a head's stats start 8-B but not 16-B aligned) with
+    256 < chunks <= 512 per sequence (the sampler's paired 16-B stats loads): parity with the oracle."""
+    inp = to_cuda(si.make_decode_inputs(3, 16, 4, 128, [20000, 16447, 19000], dtype="bf16", seed=63))
+    out, idx = gpu_decode(inp, 192, "stratified", seed=5)
+    REPORT.append(("odd-Cmax", 0, "auto", check_parity(inp, out, idx, 192, "stratified", 5)))
