@@ -247,4 +247,144 @@ __global__ void __launch_bounds__(kScoreThreads, (sizeof(T) == 2 && G <= 4) ? 8 
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// bern_stream_kernel: the Bernoulli score stage as a PERSISTENT stream (decode, 16-bit caches).
+// The feature-major rows of the selected features are read key-block by key-block: work item =
+// (unit, 2048 keys), warp w owns keys [256 w, 256 w + 256) of the block (lane l: 8 keys = one
+// 16-B load per feature row) and loops over ALL selected features, so a warp's accumulators are
+// final when its loop ends (no cross-warp reduction, no per-chunk CTA launch: the CTA-per-256-key
+// kernel above ran ~16k short CTAs at 0.48-0.51 of peak).  Loads are software-pipelined UF
+// features ahead in a register ring (UF * 512 B in flight per warp; 2 CTAs x 8 warps per SM).
+// Items are interleaved over the grid; a CTA re-reads the weights / selection into shared memory
+// when its next item belongs to another unit.  Epilogue: the L = 64 register
+// epilogue of the exact score pass on each of the warp's four 64-key sub-chunks -> the sampler's
+// stash / chunk stats layout (sub64), unchanged downstream.
+constexpr int kBernStreamWarps = 8;
+constexpr int kBernBlockKeys = kBernStreamWarps * 256;
+
+template <typename T, int D, int G>
+__global__ void __launch_bounds__(32 * kBernStreamWarps, 2) bern_stream_kernel(BernParams p, int items) {
+  static_assert(sizeof(T) == 2, "16-bit caches");
+  constexpr int UF = 16;
+  __shared__ __align__(16) float sW[D][G];               // weights, feature-major
+  __shared__ int sSel[D];
+  __shared__ __align__(16) float sS[kBernStreamWarps][G * 64];  // one 64-key sub-chunk per warp at a time
+  pdl_wait_primary();
+  pdl_launch_dependents();
+  if (blockIdx.x == 0 && threadIdx.x == 0 && p.flags) *p.flags = 0u;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nblk = (p.score_stride + kBernBlockKeys - 1) / kBernBlockKeys;  // key blocks per unit (max_seqlen)
+  // items interleaved over the grid (item t on CTA t % grid): the CTAs in flight cover whole units,
+  // so every selected feature row is read along its full length by many CTAs at once (DRAM page
+  // locality; a contiguous item range per CTA scattered the reads over ~27k open rows: 0.25 of peak)
+  const int P = p.page_table ? p.page_size : p.score_stride;
+  const float sl2 = p.scale * kLog2e;
+  int cur_unit = -1, nsel = 0;
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    const int unit = it / nblk, blk = it - unit * nblk;
+    const int b = unit / p.Hkv, kvh = unit - b * p.Hkv;
+    const size_t bh0 = (size_t)b * p.H + (size_t)kvh * G;
+    const int seqlen = __ldg(p.seqlens + b);
+    const int blk_start = blk * kBernBlockKeys;
+    if (blk_start >= seqlen) {  // whole block past the sequence: empty sub-chunk stats
+      for (int t = threadIdx.x; t < G * (kBernBlockKeys / 64); t += blockDim.x) {
+        const int c = blk_start / 64 + t % (kBernBlockKeys / 64);
+        if (c < p.Cmax) p.cstats[(bh0 + t / (kBernBlockKeys / 64)) * p.Cmax + c] = make_float2(-INFINITY, 0.f);
+      }
+      continue;
+    }
+    if (unit != cur_unit) {  // (uniform over the CTA)
+      __syncthreads();       // every warp is done with the previous unit's tables
+      nsel = p.sel_n[unit];
+      for (int t = threadIdx.x; t < G * D; t += blockDim.x) {
+        const int g = t / D, i = t - g * D;
+        sW[i][g] = p.w[(size_t)unit * G * D + t];
+      }
+      for (int t = threadIdx.x; t < nsel; t += blockDim.x) sSel[t] = p.sel[(size_t)unit * D + t];
+      __syncthreads();
+      cur_unit = unit;
+    }
+    // this lane's 8 keys
+    const int k0 = blk_start + 256 * warp + 8 * lane;
+    const bool live = k0 < seqlen;
+    const int page = k0 / P, within = k0 - page * P;
+    const int64_t phys = p.page_table ? (int64_t)__ldg(p.page_table + (int64_t)b * p.max_pages + page) : b;
+    const T* Kt = reinterpret_cast<const T*>(p.Kt) + ((phys * p.Hkv + kvh) * D) * (int64_t)P + within;
+    float acc[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+    // two batches of UB feature rows in flight: issue batch k+1, then consume batch k (the loads of a
+    // batch complete on one scoreboard -- a 16-deep single ring shared scoreboards between old and
+    // freshly issued loads and waited a full DRAM latency per row: 0.25 of peak, ncu long_scoreboard)
+    constexpr int UB = UF / 2;
+    uint4 ra[UB], rb[UB];
+    auto issue = [&](uint4 (&r)[UB], int s0) {
+#pragma unroll
+      for (int u = 0; u < UB; ++u)
+        r[u] = (live && s0 + u < nsel) ? ldg_stream(Kt + (int64_t)sSel[s0 + u] * P) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    auto consume = [&](const uint4 (&r)[UB], int s0) {
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int s = s0 + u;
+        if (s >= nsel) break;
+        const int i = sSel[s];
+        const float4 w4 = *reinterpret_cast<const float4*>(&sW[i][0]);
+        const float wg[4] = {w4.x, w4.y, w4.z, w4.w};
+        const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+        float v[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[2 * e] = Elem<T>::lo(wv[e]);
+          v[2 * e + 1] = Elem<T>::hi(wv[e]);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float wgt = G <= 4 ? wg[g] : sW[i][g];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(wgt, v[e], acc[g][e]);
+        }
+      }
+    };
+    issue(ra, 0);
+    for (int s0 = 0; s0 < nsel; s0 += UF) {
+      issue(rb, s0 + UB);
+      consume(ra, s0);
+      issue(ra, s0 + UF);
+      consume(rb, s0 + UB);
+    }
+    // epilogue: the warp's 4 sub-chunks of 64 keys, each through smem [G][64]
+#pragma unroll
+    for (int sub = 0; sub < 4; ++sub) {
+      const int sub_start = blk_start + 256 * warp + 64 * sub;
+      const int n_sub = min(64, seqlen - sub_start);
+      // lanes 8 sub .. 8 sub + 7 hold this sub-chunk's keys
+      if ((lane >> 3) == sub) {
+        const int kk = 8 * (lane & 7);
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const bool valid = kk + e < n_sub;
+            sS[warp][g * 64 + kk + e] = valid ? acc[g][e] * sl2 : -INFINITY;
+            if (p.scores && sub_start + kk + e < p.score_stride)
+              p.scores[(bh0 + g) * p.score_stride + sub_start + kk + e] = valid ? acc[g][e] * p.scale : 0.f;
+          }
+      }
+      __syncwarp();
+      const int c = sub_start / 64;
+      if (n_sub > 0) {
+        if (p.stash)
+          warp_chunk_epilogue<G>(sS[warp], 64, n_sub, p.stash + bh0 * p.stash_stride + sub_start, p.stash_stride,
+                                 p.cstats + bh0 * p.Cmax + c, p.Cmax);
+      } else if (lane < G && c < p.Cmax) {
+        p.cstats[(bh0 + lane) * p.Cmax + c] = make_float2(-INFINITY, 0.f);
+      }
+      __syncwarp();
+    }
+  }
+}
+
 }  // namespace santa

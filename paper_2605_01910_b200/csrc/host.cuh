@@ -2,6 +2,7 @@
 // per-(family, dtype, head_dim) kernel-instantiation units (inst.cu): workspace layout, launch
 // helpers, per-device attribute caches, tensor-map encoding, and the launcher declarations.
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdio>

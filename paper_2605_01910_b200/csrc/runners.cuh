@@ -41,8 +41,10 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
 template <typename T, int D, int G>
 santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   SampleParams p = make_sample_params(a);
-  if (p.L == 64 && a.stats_all == nullptr) {  // the low-latency sampler (sample_fast.cuh)
-    const int heads = a.g->batch * a.g->n_heads;
+  // the low-latency sampler (sample_fast.cuh) when its grid is one wave (its CTAs hold one SM each);
+  // beyond that the 256-thread cluster sampler below is faster (config 5, batch 16: 61 vs ~33 us)
+  const int heads = a.g->batch * a.g->n_heads;
+  if (p.L == 64 && a.stats_all == nullptr && heads <= num_sms()) {
     // CTAs per head: up to a 4-CTA cluster while the grid stays one wave (config 2: 32 heads x 4;
     // tools/tail_sweep.py: CS = 1 / 2 / 4 -> 26.8 / 24.6 / 22.6 us per step), >= 8 strata per CTA
     int CS = 1;
@@ -77,7 +79,6 @@ santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   // CTAs per head: a thread-block cluster of CS CTAs splits the S strata (more SMs on the
   // latency-bound search/gather), partials summed through DSMEM.  Aim at >= ~2 CTAs per SM.
   int CS = 1;
-  const int heads = a.g->batch * a.g->n_heads;
   while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
   p.cluster = CS;
   const size_t smem = sample_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
@@ -348,6 +349,17 @@ santa_status RunBern<T, D, G>::run(const DecodeArgs& a, const void* Kt, int nB, 
   if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
       cudaSuccess)
     return SANTA_ERR_CUDA;
+  if constexpr (sizeof(T) == 2) {
+    if (for_decode && p.sub64) {  // decode on 64-key chunks: the persistent stream (bern_stream_kernel)
+      const int nblk = (a.g->max_seqlen + kBernBlockKeys - 1) / kBernBlockKeys;
+      const int items = a.g->batch * a.g->n_kv_heads * nblk;
+      const int grid = std::min(items, 2 * num_sms());
+      if (launch(bern_stream_kernel<T, D, G>, dim3(grid), dim3(32 * kBernStreamWarps), 0, a.st, true, p, items) !=
+          cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
+    }
+  }
   if (launch(bern_chunk_kernel<T, D, G>, dim3(a.L.Cmax256, a.g->n_kv_heads, a.g->batch), dim3(kScoreThreads), 0,
              a.st, true, p) != cudaSuccess)
     return SANTA_ERR_CUDA;

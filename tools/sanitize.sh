@@ -7,7 +7,7 @@ for tool in memcheck racecheck synccheck; do
   for part in decode prop flash dense bernoulli seqshard host; do
     timeout 900 $CS --tool $tool --error-exitcode 0 --print-limit 50 python tools/sanitize_driver.py $part \
       > $O/${tool}_${part}.log 2>&1
-    echo "$tool $part: $(grep -h 'ERROR SUMMARY' $O/${tool}_${part}.log | tail -1)" >> $O/summary.txt
+    echo "$tool $part: $(grep -h 'SUMMARY' $O/${tool}_${part}.log | tail -1)" >> $O/summary.txt
   done
 done
 cat $O/summary.txt
