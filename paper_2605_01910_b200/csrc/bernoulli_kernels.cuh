@@ -247,6 +247,21 @@ __global__ void __launch_bounds__(kScoreThreads, (sizeof(T) == 2 && G <= 4) ? 8 
   }
 }
 
+__device__ __forceinline__ unsigned long long pack_f32x2(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void unpack_f32x2(unsigned long long v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+// d = a * b + c on both fp32 lanes of b / c, a broadcast (fma.rn.f32x2, sm_100 FFMA2)
+__device__ __forceinline__ unsigned long long ffma2_bcast(float a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pack_f32x2(a, a)), "l"(b), "l"(c));
+  return r;
+}
+
 // ---------------------------------------------------------------------------------------
 // bern_stream_kernel: the Bernoulli score stage as a PERSISTENT stream (decode, 16-bit caches).
 // The feature-major rows of the selected features are read key-block by key-block: work item =
@@ -310,11 +325,11 @@ __global__ void __launch_bounds__(32 * kBernStreamWarps, 2) bern_stream_kernel(B
     const int page = k0 / P, within = k0 - page * P;
     const int64_t phys = p.page_table ? (int64_t)__ldg(p.page_table + (int64_t)b * p.max_pages + page) : b;
     const T* Kt = reinterpret_cast<const T*>(p.Kt) + ((phys * p.Hkv + kvh) * D) * (int64_t)P + within;
-    float acc[G][8];
+    unsigned long long acc2[G][4];  // fp32 pairs: keys (2e, 2e+1)
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[g][e] = 0.f;
+      for (int e = 0; e < 4; ++e) acc2[g][e] = 0ull;
     // two batches of UB feature rows in flight: issue batch k+1, then consume batch k (the loads of a
     // batch complete on one scoreboard -- a 16-deep single ring shared scoreboards between old and
     // freshly issued loads and waited a full DRAM latency per row: 0.25 of peak, ncu long_scoreboard)
@@ -325,6 +340,8 @@ __global__ void __launch_bounds__(32 * kBernStreamWarps, 2) bern_stream_kernel(B
       for (int u = 0; u < UB; ++u)
         r[u] = (live && s0 + u < nsel) ? ldg_stream(Kt + (int64_t)sSel[s0 + u] * P) : make_uint4(0u, 0u, 0u, 0u);
     };
+    // the FMAs as packed fp32x2 (FFMA2, sm_100: two keys per instruction, the weight broadcast; each
+    // lane is an IEEE fma, bit-identical to fmaf): the kernel was issue-bound on 32 FFMA per row segment
     auto consume = [&](const uint4 (&r)[UB], int s0) {
 #pragma unroll
       for (int u = 0; u < UB; ++u) {
@@ -334,17 +351,14 @@ __global__ void __launch_bounds__(32 * kBernStreamWarps, 2) bern_stream_kernel(B
         const float4 w4 = *reinterpret_cast<const float4*>(&sW[i][0]);
         const float wg[4] = {w4.x, w4.y, w4.z, w4.w};
         const uint32_t wv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
-        float v[8];
+        unsigned long long v2[4];  // keys (2e, 2e+1) as an fp32 pair
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          v[2 * e] = Elem<T>::lo(wv[e]);
-          v[2 * e + 1] = Elem<T>::hi(wv[e]);
-        }
+        for (int e = 0; e < 4; ++e) v2[e] = pack_f32x2(Elem<T>::lo(wv[e]), Elem<T>::hi(wv[e]));
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const float wgt = G <= 4 ? wg[g] : sW[i][g];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[g][e] = fmaf(wgt, v[e], acc[g][e]);
+          for (int e = 0; e < 4; ++e) acc2[g][e] = ffma2_bcast(wgt, v2[e], acc2[g][e]);
         }
       }
     };
@@ -355,6 +369,11 @@ __global__ void __launch_bounds__(32 * kBernStreamWarps, 2) bern_stream_kernel(B
       issue(ra, s0 + UF);
       consume(rb, s0 + UB);
     }
+    float acc[G][8];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) unpack_f32x2(acc2[g][e], acc[g][2 * e], acc[g][2 * e + 1]);
     // epilogue: the warp's 4 sub-chunks of 64 keys, each through smem [G][64]
 #pragma unroll
     for (int sub = 0; sub < 4; ++sub) {
