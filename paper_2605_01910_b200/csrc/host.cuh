@@ -45,6 +45,7 @@ struct WsLayout {
   int L = 64, Cmax = 0, Cmax256 = 0;
   size_t stash = 0, cstats = 0, tickets = 0, flags = 0, sync = 0, bern = 0, total = 0;
   size_t step_rec = 0, step_stash = 0, step_part = 0;  // step kernel's tagged regions
+  size_t dense_o = 0, dense_ml = 0;  // dense_split_kernel partials
 };
 
 constexpr int kMaxSeqlen = 1 << 20;   // chunk-CDF tables are sized for <= 8192 chunks of <= 128 keys
@@ -100,6 +101,9 @@ inline WsLayout layout(const santa_geometry* g, int S) {
   L.step_rec = off; off = align256(off + B * H * (size_t)L.Cmax * 16);
   L.step_stash = off; off = align256(off + B * H * (size_t)L.Cmax * 64 * 4);
   L.step_part = off; off = align256(off + B * H * (size_t)kStepMaxSplits * D * 8);
+  const size_t dslots = ((size_t)kDenseSplitMaxCtas + B * Hkv) * kDenseWarps;  // dense_split_kernel slots
+  L.dense_o = off; off = align256(off + dslots * G * D * 4);
+  L.dense_ml = off; off = align256(off + dslots * G * 8);
   L.total = off;
   return L;
 }

@@ -265,18 +265,19 @@ santa_status RunDense<T, D, G>::run(const DecodeArgs& a) {
   p.flags = at<uint32_t>(a.ws, a.L.flags);
   bool done = false;
   if constexpr (sizeof(T) == 2) {
-    if (stream_eligible(a.g)) {  // tensor-core streaming flash-decoding kernel
+    if (stream_eligible(a.g)) {  // balanced split-KV tensor-core kernel + its LSE combine
       constexpr int NW = kDenseWarps, SPW = kDenseSlots;
       constexpr size_t kStageBytes = 2 * (D / 64) * kDenseStageKeys * 128;
       const size_t smem = 1024 + (size_t)NW * SPW * (kStageBytes + 16) + (size_t)NW * 8 * kPRow * 2;
-      if (ensure_smem(dense_stream_kernel<T, D, G, NW, SPW>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+      auto kern = dense_split_kernel<T, D, G, NW, SPW>;
+      if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
       CUtensorMap tk, tv;
       const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
                                             : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
       if (!make_kmap(&tk, a.K, rows, D, a.g->dtype, kDenseStageKeys) ||
           !make_kmap(&tv, a.V, rows, D, a.g->dtype, kDenseStageKeys))
         return SANTA_ERR_CUDA;
-      DenseStreamParams dp;
+      DenseSplitParams dp;
       dp.q = a.q;
       dp.kv = p.kv;
       dp.seqlens = a.seqlens;
@@ -284,16 +285,17 @@ santa_status RunDense<T, D, G>::run(const DecodeArgs& a) {
       dp.H = p.H;
       dp.Hkv = p.Hkv;
       dp.scale_log2 = p.scale_log2;
-      dp.cstats = p.cstats;
-      dp.opart = p.opart;
-      dp.Cmax = p.Cmax;
+      dp.part_o = at<float>(a.ws, a.L.dense_o);
+      dp.part_ml = at<float2>(a.ws, a.L.dense_ml);
+      dp.out = a.out;
       dp.flags = p.flags;
-      const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
-      const int grid = total < num_sms() ? total : num_sms();
-      if (launch(dense_stream_kernel<T, D, G, NW, SPW>, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv,
-                 dp) != cudaSuccess)
+      const int grid = std::min(num_sms(), kDenseSplitMaxCtas);
+      if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv, dp) != cudaSuccess)
         return SANTA_ERR_CUDA;
-      done = true;
+      if (launch(dense_split_combine<T, D, G, NW>, dim3(a.g->n_heads, a.g->batch), dim3(512), 0, a.st, true, dp,
+                 grid) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
     }
   }
   if (!done) {
