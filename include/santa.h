@@ -331,6 +331,43 @@ santa_status santa_decode_step_host_packed(const santa_geometry* geo, const void
                                            void* out_host, void* workspace, size_t workspace_bytes,
                                            int32_t synchronize, void* stream);
 
+/* Decode-loop integration.
+ *
+ * santa_decode_attention_append: the decode step WITH the KV append of the current token, the way
+ * FA-2's decode kernel appends: k_new / v_new are device [batch, n_kv_heads,
+ * head_dim] rows (dtype of the cache, 16-B aligned) written into K / V (now writable) at slot
+ * seqlens[b] - 1 (seqlens include the new token, reading #10), then the step of
+ * santa_decode_attention.  On the two-kernel path (AUTO below 1024 query heads) the append is fused
+ * into the score pass: the TMA producer lane that streams the stage holding the slot writes both
+ * rows first (then a generic->async proxy fence, so its own TMA load sees the new key); on the
+ * single-launch step kernels and the fp32 / odd-page fallback a one-CTA-per-(b, kv head) append
+ * kernel runs first.  Same validation, errors and determinism as santa_decode_attention (nothing
+ * is written on error).
+ *
+ * Per-layer budgets (App. K: a learned schedule assigns each transformer layer its own
+ * S under a global budget): santa_layer_schedule is a HOST array S[n_layers] (each >= 1, <= 4096).
+ * santa_decode_attention_layer decodes layer `layer` with S = sched->S[layer] and the Philox
+ * offset (offset * n_layers + layer), so every (step, layer) has its own stream; k_new / v_new
+ * may be NULL (no append) or the new token's rows (append as above).  idx_out rows are
+ * sched->S[layer] long.  santa_schedule_workspace_bytes = the workspace for every layer of the
+ * schedule (the max over its S; one workspace serves all layers of a stream in turn). */
+typedef struct santa_layer_schedule {
+  int32_t n_layers;
+  const int32_t* S; /* host [n_layers] */
+} santa_layer_schedule;
+
+santa_status santa_decode_attention_append(const santa_geometry* geo, const void* q, void* K, void* V,
+                                           const void* k_new, const void* v_new, const int32_t* seqlens,
+                                           int32_t S, int32_t mode, uint64_t seed, uint64_t offset, void* out,
+                                           int32_t* idx_out, void* workspace, size_t workspace_bytes,
+                                           void* stream);
+size_t santa_schedule_workspace_bytes(const santa_geometry* geo, const santa_layer_schedule* sched);
+santa_status santa_decode_attention_layer(const santa_geometry* geo, const santa_layer_schedule* sched,
+                                          int32_t layer, const void* q, void* K, void* V, const void* k_new,
+                                          const void* v_new, const int32_t* seqlens, int32_t mode,
+                                          uint64_t seed, uint64_t offset, void* out, int32_t* idx_out,
+                                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Device Philox4x32-10 uniforms for testing the device RNG against the Random123 KAT and
  * the oracle stream: out[i] = u(draw i) of the stream (seed, offset, tag, h_global, b_global),
  * u = r * 2^-32 (reading #1).  out is device fp64 [n]; if raw_out != NULL it receives the 4

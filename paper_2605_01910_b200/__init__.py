@@ -16,7 +16,7 @@ from typing import Optional, Sequence
 import torch
 
 from . import _abi
-from ._abi import DTYPES, FLAG_EMPTY_SEQ, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry, SantaError
+from ._abi import DTYPES, FLAG_EMPTY_SEQ, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry, LayerSchedule, SantaError
 
 __all__ = [
     "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes", "santa_auto_path",
@@ -27,6 +27,8 @@ __all__ = [
     "santa_bernoulli_scores", "santa_decode_attention_bernoulli", "santa_seqshard_stats",
     "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_decode_step_host_packed", "santa_philox_uniforms",
     "santa_read_error_flags", "santa_version", "decode", "decode_prop", "dense", "LIB_PATH",
+    "santa_decode_attention_append", "LayerSchedule", "make_schedule", "santa_schedule_workspace_bytes",
+    "santa_decode_attention_layer", "decode_append",
 ]
 LIB_PATH = _abi.LIB_PATH
 _TORCH_DT = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float16: "f16"}
@@ -210,6 +212,38 @@ def santa_decode_step_host_packed(geo, qkv_host, qkv_dev, K, V, seqlens, S, mode
         seed, offset, _ptr(out_dev), hp(out_host), _ptr(ws), ws.numel(), int(bool(synchronize)), _stream(stream)))
 
 
+def santa_decode_attention_append(geo, q, K, V, k_new, v_new, seqlens, S, mode, seed, offset, out, idx_out, ws,
+                                  stream=None):
+    """Decode step with the current token's KV append (k_new / v_new [B, H_kv, d] written at slot
+    seqlens[b] - 1 of K / V; fused into the score pass on the two-kernel path; include/santa.h)."""
+    _abi.check("santa_decode_attention_append", _abi.LIB.santa_decode_attention_append(
+        ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(k_new), _ptr(v_new), _ptr(seqlens), S,
+        MODES.get(mode, mode), seed, offset, _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def make_schedule(S_per_layer: Sequence[int]) -> LayerSchedule:
+    """Per-layer sample budgets (App. K): a santa_layer_schedule over a host int32 array.  The array
+    is kept alive on the returned struct."""
+    arr = (ctypes.c_int32 * len(S_per_layer))(*[int(x) for x in S_per_layer])
+    sched = LayerSchedule(len(S_per_layer), ctypes.cast(arr, ctypes.POINTER(ctypes.c_int32)))
+    sched._keep = arr
+    return sched
+
+
+def santa_schedule_workspace_bytes(geo: Geometry, sched: LayerSchedule) -> int:
+    return int(_abi.LIB.santa_schedule_workspace_bytes(ctypes.byref(geo), ctypes.byref(sched)))
+
+
+def santa_decode_attention_layer(geo, sched, layer, q, K, V, k_new, v_new, seqlens, mode, seed, offset, out,
+                                 idx_out, ws, stream=None):
+    """Layer `layer` of a per-layer schedule: S = sched.S[layer], Philox offset offset*n_layers+layer;
+    k_new / v_new None (no append) or the new token's rows."""
+    _abi.check("santa_decode_attention_layer", _abi.LIB.santa_decode_attention_layer(
+        ctypes.byref(geo), ctypes.byref(sched), layer, _ptr(q), _ptr(K), _ptr(V), _ptr(k_new), _ptr(v_new),
+        _ptr(seqlens), MODES.get(mode, mode), seed, offset, _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(),
+        _stream(stream)))
+
+
 def santa_philox_uniforms(seed, offset, tag, h_global, b_global, n, out, ctr_key: Optional[Sequence[int]] = None,
                           raw_out=None, stream=None):
     ck = (ctypes.c_uint32 * 6)(*ctr_key) if ctr_key is not None else None
@@ -307,3 +341,19 @@ def dense(q, K, V, seqlens, n_kv_heads=None, page_table=None, page_size=0, max_s
     out = torch.empty_like(q)
     santa_dense_reference(geo, q, K, V, seqlens, out, ws)
     return out
+
+
+def decode_append(q, K, V, k_new, v_new, seqlens, S, mode="stratified", seed=0, offset=0, return_idx=False, ws=None):
+    """Allocate out (+ idx) and workspace, run santa_decode_attention_append on a contiguous cache."""
+    Hkv = K.shape[1]
+    _check_cache(q, K, V, Hkv, K.shape[2], None, 0)
+    if k_new.shape != (q.shape[0], Hkv, q.shape[2]) or v_new.shape != k_new.shape or k_new.dtype != q.dtype:
+        raise ValueError("k_new / v_new must be [B, H_kv, d] of the cache dtype")
+    geo = make_geometry(q, Hkv, K.shape[2])
+    if ws is None:
+        ws = workspace(geo, S, q.device)
+    out = torch.empty_like(q)
+    idx = torch.empty((q.shape[0], q.shape[1], S), dtype=torch.int32, device=q.device) if return_idx else None
+    santa_decode_attention_append(geo, q, K, V, k_new.contiguous(), v_new.contiguous(), seqlens, S, mode, seed,
+                                  offset, out, idx, ws)
+    return (out, idx) if return_idx else out

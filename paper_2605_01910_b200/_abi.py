@@ -27,6 +27,10 @@ class SantaError(RuntimeError):
         self.status = status
 
 
+class LayerSchedule(ctypes.Structure):
+    _fields_ = [("n_layers", ctypes.c_int32), ("S", ctypes.POINTER(ctypes.c_int32))]
+
+
 class Geometry(ctypes.Structure):
     _fields_ = [
         ("batch", ctypes.c_int32),
@@ -76,6 +80,10 @@ def _load() -> ctypes.CDLL:
         "santa_decode_step_host_packed": ([G, vp, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, i32, vp], i32),
         "santa_philox_uniforms": ([u64, u64, i32, i32, i32, i32, vp, vp, vp, vp], i32),
         "santa_read_error_flags": ([vp, ctypes.POINTER(ctypes.c_uint32), vp], i32),
+        "santa_decode_attention_append": ([G, vp, vp, vp, vp, vp, vp, i32, i32, u64, u64, vp, vp, vp, sz, vp], i32),
+        "santa_schedule_workspace_bytes": ([G, ctypes.POINTER(LayerSchedule)], sz),
+        "santa_decode_attention_layer": ([G, ctypes.POINTER(LayerSchedule), i32, vp, vp, vp, vp, vp, vp, i32, u64,
+                                          u64, vp, vp, vp, sz, vp], i32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)

@@ -201,6 +201,10 @@ struct DecodeArgs {
   const int32_t* token_offset;
   int Lc = 0, Cc = 0;         // chunking the sampler reads (0 => the SANTA layout L / Cmax)
   bool tensor_core = false;   // step kernel: score stage on tcgen05 (step_tc_kernel.cuh)
+  const void* k_new = nullptr;  // fused KV append (two-kernel path's score pass)
+  const void* v_new = nullptr;
+  void* K_w = nullptr;
+  void* V_w = nullptr;
 };
 
 // ---- host-side caches: per device, safe under concurrent calls from several host threads ----
@@ -329,6 +333,10 @@ inline ScoreParams make_score_params(const DecodeArgs& a) {
   p.stash_stride = a.L.Cmax * a.L.L;
   p.tickets = at<uint32_t>(a.ws, a.L.tickets);
   p.flags = at<uint32_t>(a.ws, a.L.flags);
+  p.k_new = a.k_new;
+  p.v_new = a.v_new;
+  p.K_w = a.K_w;
+  p.V_w = a.V_w;
   return p;
 }
 

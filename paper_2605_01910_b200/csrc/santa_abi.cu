@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -534,6 +535,72 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
     return SANTA_ERR_CUDA;
   if (synchronize && cudaStreamSynchronize(st) != cudaSuccess) return SANTA_ERR_CUDA;
   return SANTA_OK;
+}
+
+// decode step with the current token's KV append (fused into the score pass on the two-kernel path)
+static santa_status decode_append(const santa_geometry* g, const void* q, void* K, void* V, const void* k_new,
+                                  const void* v_new, const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
+                                  uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+  DecodeArgs a;
+  santa_status s = prepare_decode(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr,
+                                  stream, SANTA_PATH_AUTO, &a);
+  if (s != SANTA_OK) return s;
+  if (!k_new || !v_new) return SANTA_ERR_INVALID_ARG;
+  if (!aligned16(k_new) || !aligned16(v_new)) return SANTA_ERR_ALIGNMENT;
+  const int G = g->n_heads / g->n_kv_heads;
+  if (auto_path(g, S) == SANTA_PATH_TWO_KERNEL && stream_eligible(g) && a.L.L == 64) {
+    a.k_new = k_new;
+    a.v_new = v_new;
+    a.K_w = K;
+    a.V_w = V;
+    if ((s = dispatch<RunScore>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+    if ((s = dispatch<RunSample>(g->dtype, g->head_dim, G, a)) != SANTA_OK) return s;
+    return last_cuda();
+  }
+  const int eb = elem_bytes(g->dtype);
+  append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, a.st>>>(K, V, k_new, v_new, kv_layout(g), seqlens,
+                                                                    g->head_dim, eb);
+  if ((s = last_cuda()) != SANTA_OK) return s;
+  return run_decode(a, SANTA_PATH_AUTO);
+}
+
+santa_status santa_decode_attention_append(const santa_geometry* g, const void* q, void* K, void* V,
+                                           const void* k_new, const void* v_new, const int32_t* seqlens, int32_t S,
+                                           int32_t mode, uint64_t seed, uint64_t offset, void* out,
+                                           int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  return decode_append(g, q, K, V, k_new, v_new, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, stream);
+}
+
+static santa_status check_schedule(const santa_layer_schedule* sched) {
+  if (!sched || !sched->S || sched->n_layers < 1) return SANTA_ERR_INVALID_ARG;
+  for (int l = 0; l < sched->n_layers; ++l) {
+    if (sched->S[l] < 1) return SANTA_ERR_EMPTY_BUDGET;
+    if (sched->S[l] > kMaxBudget) return SANTA_ERR_UNSUPPORTED;
+  }
+  return SANTA_OK;
+}
+
+size_t santa_schedule_workspace_bytes(const santa_geometry* g, const santa_layer_schedule* sched) {
+  if (validate_geometry(g) != SANTA_OK || check_schedule(sched) != SANTA_OK) return 0;
+  size_t m = 0;
+  for (int l = 0; l < sched->n_layers; ++l) m = std::max(m, layout(g, sched->S[l]).total);
+  return m;
+}
+
+santa_status santa_decode_attention_layer(const santa_geometry* g, const santa_layer_schedule* sched, int32_t layer,
+                                          const void* q, void* K, void* V, const void* k_new, const void* v_new,
+                                          const int32_t* seqlens, int32_t mode, uint64_t seed, uint64_t offset,
+                                          void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  santa_status s = check_schedule(sched);
+  if (s != SANTA_OK) return s;
+  if (layer < 0 || layer >= sched->n_layers) return SANTA_ERR_INVALID_ARG;
+  if ((k_new == nullptr) != (v_new == nullptr)) return SANTA_ERR_INVALID_ARG;
+  const int32_t S = sched->S[layer];
+  const uint64_t off = offset * (uint64_t)sched->n_layers + (uint64_t)layer;
+  if (k_new)
+    return decode_append(g, q, K, V, k_new, v_new, seqlens, S, mode, seed, off, out, idx_out, ws, ws_bytes, stream);
+  return decode_common(g, q, K, V, seqlens, S, mode, seed, off, out, idx_out, ws, ws_bytes, nullptr, stream);
 }
 
 santa_status santa_philox_uniforms(uint64_t seed, uint64_t offset, int32_t tag, int32_t h_global, int32_t b_global,

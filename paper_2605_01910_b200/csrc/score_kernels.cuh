@@ -45,6 +45,13 @@ struct ScoreParams {
   int stash_stride;         // Cmax * L
   uint32_t* tickets;        // [B * Hkv], zeroed here for the sample kernel
   uint32_t* flags;          // zeroed here
+  // fused KV append (santa_decode_attention_append; NULL = none): the new token's rows
+  // k_new / v_new [B, Hkv, D] are written into K_w / V_w (the caches K / V, writable) at slot
+  // seqlens[b] - 1 by the producer lane that streams that slot's stage, before its TMA load
+  const void* k_new;
+  const void* v_new;
+  void* K_w;
+  void* V_w;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -342,6 +349,25 @@ __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const
             row = (int32_t)((phys * p.Hkv + kvh) * p.kv.page_size + within);
           } else {
             row = cw[j].unit * p.kv.page_size + t;  // contiguous [B*Hkv][max_seqlen] rows
+          }
+          if (p.k_new) {  // fused append: the new token lands in this stage -> write it first
+            const int b = cw[j].unit / p.Hkv;
+            const int tnew = __ldg(p.seqlens + b) - 1;
+            if (tnew >= t && tnew < t + kStageKeys) {
+              const int64_t drow = (int64_t)row + (tnew - t);  // cache row of the new token (pages hold
+              const int64_t srow = cw[j].unit;                 // whole 64-key stages: same page)
+              const uint4* ks = reinterpret_cast<const uint4*>(p.k_new) + srow * (D * sizeof(T) / 16);
+              const uint4* vs = reinterpret_cast<const uint4*>(p.v_new) + srow * (D * sizeof(T) / 16);
+              uint4* kd = reinterpret_cast<uint4*>(p.K_w) + drow * (D * sizeof(T) / 16);
+              uint4* vd = reinterpret_cast<uint4*>(p.V_w) + drow * (D * sizeof(T) / 16);
+#pragma unroll
+              for (int i = 0; i < (int)(D * sizeof(T) / 16); ++i) {
+                kd[i] = __ldg(ks + i);
+                vd[i] = __ldg(vs + i);
+              }
+              // the generic-proxy stores of the K row must be visible to this thread's TMA (async proxy)
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
           }
           mbar_arrive_expect_tx(&full[slot], kStageBytes);
 #pragma unroll

@@ -165,3 +165,15 @@ def test_wrappers_refuse_mismatched_cache_shapes():
         santa.decode(q, pool, pool, sl, 16, page_table=pt, page_size=64)
     with pytest.raises(ValueError, match="paged pool"):
         santa.decode(q, pool, pool, sl, 16, page_table=pt.int(), page_size=32)
+
+
+def test_layer_schedule_host_logic():
+    """Per-layer budgets (App. K): the schedule's workspace is the max over its layers' workspaces;
+    malformed schedules are refused (0 bytes) without a GPU."""
+    g = _geo()
+    sched = santa.make_schedule([8, 256, 64, 1024])
+    want = max(santa.santa_workspace_bytes(g, S) for S in (8, 256, 64, 1024))
+    assert santa.santa_schedule_workspace_bytes(g, sched) == want
+    assert santa.santa_schedule_workspace_bytes(g, santa.make_schedule([8, 0])) == 0       # S < 1
+    assert santa.santa_schedule_workspace_bytes(g, santa.make_schedule([8, 5000])) == 0    # S > 4096
+    assert santa.santa_schedule_workspace_bytes(_geo(head_dim=96), sched) == 0
