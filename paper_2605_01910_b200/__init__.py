@@ -28,7 +28,7 @@ __all__ = [
     "santa_seqshard_sample_gather", "santa_decode_step_host", "santa_decode_step_host_packed", "santa_philox_uniforms",
     "santa_read_error_flags", "santa_version", "decode", "decode_prop", "dense", "LIB_PATH",
     "santa_decode_attention_append", "LayerSchedule", "make_schedule", "santa_schedule_workspace_bytes",
-    "santa_decode_attention_layer", "decode_append",
+    "santa_decode_attention_layer", "decode_append", "prepare_decode",
 ]
 LIB_PATH = _abi.LIB_PATH
 _TORCH_DT = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float16: "f16"}
@@ -94,6 +94,25 @@ def santa_decode_attention(geo, q, K, V, seqlens, S, mode, seed, offset, out, id
     _abi.check("santa_decode_attention", _abi.LIB.santa_decode_attention(
         ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), S, MODES.get(mode, mode), seed, offset,
         _ptr(out), _ptr(idx_out), _ptr(ws), ws.numel(), _stream(stream)))
+
+
+def prepare_decode(geo, q, K, V, seqlens, S, mode, seed, out, idx_out, ws, path="auto", stream=None):
+    """A decode step with every argument but the Philox offset marshalled once: returns launch(offset),
+    which issues santa_decode_attention_path on the prepared buffers (the per-step host cost of a
+    decode loop drops to one ctypes call).  The tensors must stay alive and in place."""
+    fn = _abi.LIB.santa_decode_attention_path
+    args = (ctypes.byref(geo), _ptr(q), _ptr(K), _ptr(V), _ptr(seqlens), ctypes.c_int32(S),
+            ctypes.c_int32(MODES.get(mode, mode)), ctypes.c_uint64(seed))
+    tail = (_ptr(out), _ptr(idx_out), _ptr(ws), ctypes.c_size_t(ws.numel()), ctypes.c_int32(PATHS.get(path, path)),
+            _stream(stream))
+    keep = (geo, q, K, V, seqlens, out, idx_out, ws)
+
+    def launch(offset: int):
+        st = fn(*args, ctypes.c_uint64(offset), *tail)
+        if st != 0:
+            _abi.check("santa_decode_attention_path", st)
+    launch._keep = keep
+    return launch
 
 
 def santa_decode_attention_path(geo, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, path,

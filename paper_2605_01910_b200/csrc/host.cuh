@@ -291,7 +291,36 @@ inline PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // K viewed as a 2-D tensor [rows][D] (D contiguous); 64 x 64-element boxes, 128B swizzle.
+// The encoded descriptor depends only on (address, rows, D, dtype, box): a small per-thread cache of
+// the last encodings (no lock; a decode loop re-encodes nothing -- cuTensorMapEncodeTiled is ~1 us of
+// host time per call, on the critical path when steps are launched back to back).
+struct KmapKey {
+  const void* K;
+  uint64_t rows;
+  int D, dtype, box_rows;
+  bool operator==(const KmapKey& o) const {
+    return K == o.K && rows == o.rows && D == o.D && dtype == o.dtype && box_rows == o.box_rows;
+  }
+};
+inline bool make_kmap_uncached(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype, int box_rows);
 inline bool make_kmap(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype, int box_rows = 64) {
+  constexpr int kSlots = 16;
+  thread_local KmapKey keys[kSlots] = {};
+  thread_local CUtensorMap maps[kSlots];
+  thread_local int next = 0;
+  const KmapKey key{K, rows, D, dtype, box_rows};
+  for (int i = 0; i < kSlots; ++i)
+    if (keys[i] == key) {
+      *m = maps[i];
+      return true;
+    }
+  if (!make_kmap_uncached(m, K, rows, D, dtype, box_rows)) return false;
+  keys[next] = key;
+  maps[next] = *m;
+  next = (next + 1) % kSlots;
+  return true;
+}
+inline bool make_kmap_uncached(CUtensorMap* m, const void* K, uint64_t rows, int D, int dtype, int box_rows) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
@@ -333,10 +362,6 @@ inline ScoreParams make_score_params(const DecodeArgs& a) {
   p.stash_stride = a.L.Cmax * a.L.L;
   p.tickets = at<uint32_t>(a.ws, a.L.tickets);
   p.flags = at<uint32_t>(a.ws, a.L.flags);
-  p.k_new = a.k_new;
-  p.v_new = a.v_new;
-  p.K_w = a.K_w;
-  p.V_w = a.V_w;
   return p;
 }
 

@@ -19,11 +19,19 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
     constexpr int NW = kStreamWarps, SPW = kStreamSlots;
     const size_t smem = 1024 + (size_t)NW * G * p.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
     if (smem <= 220 * 1024) {  // else: per-warp score buffers too large (G * L big) -> fallback kernel
-    if (ensure_smem(score_stream_kernel<T, D, G, NW, SPW>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
     const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
     const int grid = total < num_sms() ? total : num_sms();
-    if (launch(score_stream_kernel<T, D, G, NW, SPW>, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p) !=
-        cudaSuccess)
+    if (a.k_new) {  // the fused KV append (santa_decode_attention_append)
+      auto kern = score_stream_append_kernel<T, D, G, NW, SPW>;
+      if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+      const AppendParams ap{a.k_new, a.v_new, a.K_w, a.V_w};
+      if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p, ap) != cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
+    }
+    auto kern = score_stream_kernel<T, D, G, NW, SPW>;
+    if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+    if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p) != cudaSuccess)
       return SANTA_ERR_CUDA;
     return SANTA_OK;
     }
@@ -47,10 +55,12 @@ santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   if (p.L == 64 && a.stats_all == nullptr && heads <= num_sms()) {
     // CTAs per head: up to a 4-CTA cluster while the grid stays one wave (config 2: 32 heads x 4;
     // tools/tail_sweep.py: CS = 1 / 2 / 4 -> 26.8 / 24.6 / 22.6 us per step), >= 8 strata per CTA
+    // (whole 64-strata super-blocks per CTA: the summation tree, hence the output bits, do not depend
+    // on CS -- batch x kv-head slabs of any size give the same bits)
     int CS = 1;
-    while (CS < 4 && heads * CS * 2 <= num_sms() && CS * 2 * 8 <= a.S) CS *= 2;
+    while (CS < 4 && heads * CS * 2 <= num_sms() && CS * 2 * 64 <= a.S) CS *= 2;
     p.cluster = CS;
-    const size_t smem = sample_fast_smem_bytes(p.Cmax, D, CS);
+    const size_t smem = sample_fast_smem_bytes(p.Cmax, D, CS, a.S);
     if (ensure_smem(sample_fast_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
     if (a.events) cudaEventRecord(a.events[1], a.st);
     cudaLaunchConfig_t cfg = {};

@@ -42,9 +42,11 @@ constexpr int kFastThreads = SANTA_FAST_THREADS;
 constexpr int kFastWarps = kFastThreads / 32;
 constexpr int kFastCPT = 8;  // chunks per thread held in registers (nC <= 2048); longer: two passes
 
-// shared memory: sLoc [Cmax] fp64 | sE [Cmax] fp32 | sRed [8][D] fp32 | sRecv [CS][D] fp32
-__host__ __device__ inline size_t sample_fast_smem_bytes(int Cmax, int D, int CS) {
-  return (size_t)Cmax * 8 + (size_t)((Cmax + 3) & ~3) * 4 + (size_t)kFastWarps * D * 4 + (size_t)CS * D * 4 + 64;
+// shared memory: sLoc [Cmax] fp64 | sE [Cmax] fp32 | sBlk [blocks per CTA][D] | sRecv [super-blocks][D]
+__host__ __device__ inline size_t sample_fast_smem_bytes(int Cmax, int D, int CS, int S) {
+  const int nsb = (S + 63) / 64;
+  const int nbl = 64 * ((nsb + CS - 1) / CS) / 8;
+  return (size_t)Cmax * 8 + (size_t)((Cmax + 3) & ~3) * 4 + (size_t)nbl * D * 4 + (size_t)nsb * D * 4 + 64;
 }
 
 __device__ __forceinline__ uint32_t cluster_map_u32(uint32_t smem_addr, uint32_t rank) {
@@ -63,34 +65,40 @@ __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// One round (<= 32 samples) of the warp: half-warp hw takes the samples searched by lanes
-// hw, hw + 2, ...; U in flight.  (c, y', e) come from the searching lane by shuffles.
-template <typename T, int D, int U>
-__device__ __forceinline__ void fast_gather(const SampleParams& p, int b, int kvh, size_t bh, int seqlen, int nj,
-                                            int warp, int m_lo, int lane_c, double lane_y, float lane_e, int round,
-                                            float (&acc)[(D * sizeof(T) / 16 + 15) / 16][16 / sizeof(T)]) {
+// One round of the warp: up to 4 blocks of 8 strata (block vl's strata were searched by lanes
+// 8 vl .. 8 vl + 7).  Per block, half-warp hw gathers the strata at positions hw, hw + 2, hw + 4,
+// hw + 6 in that order, the two half-warps' sums are added, and lanes 0..15 store the BLOCK SUM to
+// sBlk[block] -- a summation tree fixed by the global strata alone (CS-invariant outputs).
+template <typename T, int D>
+__device__ __forceinline__ void fast_gather_blocks(const SampleParams& p, int b, int kvh, size_t bh, int seqlen,
+                                                   int warp, int m_lo, int m_hi, int nbl, int round, int lane_c,
+                                                   double lane_y, float lane_e, float* sBlk) {
   constexpr int EB = (int)sizeof(T);
   constexpr int VCH = D * EB / 16;      // 16-B chunks per V row
   constexpr int NCH = (VCH + 15) / 16;  // chunks per lane
   constexpr int EPC = 16 / EB;          // elements per chunk
+  constexpr int U = 4;
   const int lane = threadIdx.x & 31, hw = lane >> 4, l = lane & 15;
   const unsigned hmask = 0xffffu << (lane & 16);
   const T* Vb = reinterpret_cast<const T*>(p.V);
   const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
   const float* Pbase = p.stash + bh * p.stash_stride;
-  const int jr = min(32, nj - 32 * round);
-  for (int t0 = 0; 2 * t0 < jr; t0 += U) {
+#pragma unroll 1
+  for (int vl = 0; vl < 4; ++vl) {
+    const int bl = warp + kFastWarps * (4 * round + vl);  // local block
+    if (bl >= nbl) break;                                 // (warp-uniform)
     int cc[U], nn[U], jj[U];
     double yy[U];
     float ee[U];
     float4 pv[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int jl = hw + 2 * (t0 + u);  // the lane that searched this sample
-      const int c = __shfl_sync(0xffffffffu, lane_c, jl & 31);
-      yy[u] = __shfl_sync(0xffffffffu, lane_y, jl & 31);
-      ee[u] = __shfl_sync(0xffffffffu, lane_e, jl & 31);
-      cc[u] = jl < jr ? c : -1;
+      const int pos = hw + 2 * u, jl = 8 * vl + pos;  // the lane that searched this stratum
+      const int m = m_lo + 8 * bl + pos;
+      const int c = __shfl_sync(0xffffffffu, lane_c, jl);
+      yy[u] = __shfl_sync(0xffffffffu, lane_y, jl);
+      ee[u] = __shfl_sync(0xffffffffu, lane_e, jl);
+      cc[u] = m < m_hi ? c : -1;
       nn[u] = cc[u] >= 0 ? min(64, seqlen - cc[u] * 64) : 0;
       pv[u] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
       if (cc[u] >= 0 && 4 * l < nn[u]) pv[u] = ldcg_f4(reinterpret_cast<const float4*>(Pbase + (size_t)cc[u] * 64) + l);
@@ -122,10 +130,7 @@ __device__ __forceinline__ void fast_gather(const SampleParams& p, int b, int kv
         if (on && k >= nn[u]) k = fl2 < 16 ? 4 * fl2 + cross2 : nn[u] - 1;
       }
       jj[u] = on ? cc[u] * 64 + min(k, nn[u] - 1) : -1;
-      if (on && l == 0 && p.idx_out) {
-        const int i = warp + kFastWarps * (32 * round + hw + 2 * (t0 + u));  // local stratum index
-        p.idx_out[bh * p.S + m_lo + i] = jj[u];
-      }
+      if (on && l == 0 && p.idx_out) p.idx_out[bh * p.S + m_lo + 8 * bl + hw + 2 * u] = jj[u];
     }
     uint4 raw[U][NCH];
 #pragma unroll
@@ -136,6 +141,11 @@ __device__ __forceinline__ void fast_gather(const SampleParams& p, int b, int kv
         const T* row = p.kv.page_table ? Vb + p.kv.row(b, kvh, max(jj[u], 0), D) : vbase + (int64_t)max(jj[u], 0) * D;
         raw[u][q] = (jj[u] >= 0 && ch < VCH) ? ldg_nc(row + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
       }
+    float acc[NCH][EPC];
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
@@ -154,6 +164,19 @@ __device__ __forceinline__ void fast_gather(const SampleParams& p, int b, int kv
           acc[q][3] += __uint_as_float(raw[u][q].w);
         }
       }
+#pragma unroll
+    for (int q = 0; q < NCH; ++q)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], 16);
+    if (lane < 16) {
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        const int ch = lane + 16 * q;
+        if (ch < VCH)
+#pragma unroll
+          for (int e = 0; e < EPC; ++e) sBlk[(size_t)bl * D + ch * EPC + e] = acc[q][e];
+      }
+    }
   }
 }
 
@@ -161,11 +184,37 @@ __device__ __forceinline__ void fast_gather(const SampleParams& p, int b, int kv
 #define FAST_TRACE(i) \
   if (p.trace && threadIdx.x == 0) p.trace[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 + (i)] = gtimer()
 
+// The strata split of a head over the CS CTAs of its cluster: whole super-blocks of 64 strata
+// (8 blocks of 8), rank r owning super-blocks [nsb r / CS, nsb (r + 1) / CS) -- block / super-block
+// boundaries are fixed by the global strata, so the summation tree is the same for every CS.
+struct FastSplit {
+  int m_lo, m_hi, nbl, sb_lo, nsb_local, nsb;
+  __device__ __forceinline__ FastSplit(int S, int rank, int CS) {
+    nsb = (S + 63) / 64;
+    sb_lo = (int)((long long)nsb * rank / CS);
+    const int sb_hi = (int)((long long)nsb * (rank + 1) / CS);
+    nsb_local = sb_hi - sb_lo;
+    m_lo = 64 * sb_lo;
+    m_hi = min(S, 64 * sb_hi);
+    nbl = (m_hi - m_lo + 7) / 8;
+  }
+  // this warp's blocks bl = warp + 8 nu; round rho holds nu in [4 rho, 4 rho + 4) (lane = 8 (nu - 4 rho) + pos)
+  __device__ __forceinline__ int rounds(int warp) const {
+    const int nnu = nbl > warp ? (nbl - warp + kFastWarps - 1) / kFastWarps : 0;
+    return (nnu + 3) / 4;
+  }
+  __device__ __forceinline__ int stratum(int warp, int round, int lane) const {  // -1 if none
+    const int bl = warp + kFastWarps * (4 * round + (lane >> 3));
+    const int m = m_lo + 8 * bl + (lane & 7);
+    return (bl < nbl && m < m_hi) ? m : -1;
+  }
+};
+
 struct FastSmem {
   double* sLoc;   // [Cmax] in-warp inclusive prefix of w_c
   float* sE;      // [Cmax] e_c = 2^(m_c - m_w)
-  float* sRed;    // [NW][D]
-  float* sRecv;   // [CS][D] (rank 0)
+  float* sBlk;    // [blocks of this CTA][D] block sums
+  float* sRecv;   // [super-blocks of the head][D] super-block sums (rank 0)
   float* sWm;     // [NW]
   double* sWt;    // [NW]
   int* sWl;       // [NW]
@@ -254,9 +303,8 @@ __device__ __forceinline__ void fast_body(const SampleParams& p, const FastSmem&
   const size_t bh = (size_t)b * p.H + h;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = p.S;
-  const int m_lo = (int)((long long)S * rank / CS), m_hi = (int)((long long)S * (rank + 1) / CS);
-  const int Sl = m_hi - m_lo;
-  const int nj = Sl > warp ? (Sl - warp + NW - 1) / NW : 0;  // this warp's samples i = warp + NW j
+  const FastSplit sp(S, rank, CS);
+  const int m_lo = sp.m_lo, m_hi = sp.m_hi, Sl = m_hi - m_lo;
   const PhiloxStream ps(p.seed, p.offset, kTagValueSampler, (uint32_t)(p.head_offset + h), (uint32_t)(p.batch_offset + b));
   FAST_TRACE(2);
 
@@ -324,16 +372,11 @@ __device__ __forceinline__ void fast_body(const SampleParams& p, const FastSmem&
   const int blk = 32 * per;                        // chunks per warp block
   FAST_TRACE(4);
 
-  // ---- a5 + a6: lane-per-sample search, half-warp-per-sample count + gather, rounds of 32 ------
-  float acc[NCH][EPC];
-#pragma unroll
-  for (int q = 0; q < NCH; ++q)
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
-  const int rounds = (nj + 31) / 32;
+  // ---- a5 + a6: lane-per-stratum search (4 blocks of 8 per round), block-wise gather ----------
+  const int rounds = sp.rounds(warp);
   for (int r = 0; r < rounds; ++r) {
-    const int j = 32 * r + lane;
-    const double Tm = (r == 0 || j >= nj) ? T0 : sample_threshold(p.mode, m_lo + warp + NW * j, S, ps);
+    const int mstr = sp.stratum(warp, r, lane);
+    const double Tm = (r == 0 || mstr < 0) ? T0 : sample_threshold(p.mode, mstr, S, ps);
     const double X = Tm * Z;
     // block: the first w whose end exceeds X (clamped to the last block with mass)
     int w = 0;
@@ -346,7 +389,7 @@ __device__ __forceinline__ void fast_body(const SampleParams& p, const FastSmem&
     int lane_c = 0;
     double lane_y = 0.0;
     float lane_e = 0.f;
-    if (j < nj) {
+    if (mstr >= 0) {
       const double y = (X - offw) * rw;
       const int cb = w * blk, ce = min(cb + blk, nC);
       // min{c in [cb, ce) : L_c > y} (ce if none): quaternary steps (3 independent loads each),
@@ -370,55 +413,32 @@ __device__ __forceinline__ void fast_body(const SampleParams& p, const FastSmem&
       lane_e = sm.sE[c];
     }
     if (r == 0) FAST_TRACE(5);
-    fast_gather<T, D, 4>(p, b, kvh, bh, seqlen, nj, warp, m_lo, lane_c, lane_y, lane_e, r, acc);
+    fast_gather_blocks<T, D>(p, b, kvh, bh, seqlen, warp, m_lo, m_hi, sp.nbl, r, lane_c, lane_y, lane_e, sm.sBlk);
   }
   FAST_TRACE(6);
-
-  // ---- reduction: half-warp pair (shuffle), warps (smem), ranks (DSMEM + mbarrier) -------------
-#pragma unroll
-  for (int q = 0; q < NCH; ++q)
-#pragma unroll
-    for (int e = 0; e < EPC; ++e) acc[q][e] += __shfl_xor_sync(0xffffffffu, acc[q][e], 16);
-  if (lane < 16) {
-#pragma unroll
-    for (int q = 0; q < NCH; ++q) {
-      const int ch = lane + 16 * q;
-      if (ch < VCH)
-#pragma unroll
-        for (int e = 0; e < EPC; ++e) sm.sRed[warp * D + ch * EPC + e] = acc[q][e];
-    }
-  }
   __syncthreads();
   FAST_TRACE(7);
+  // ---- reduction, fixed by the strata: super-block sum = its 8 block sums in order; the head's sum =
+  // its super-block sums in order (ranks 1..CS-1 store theirs into rank 0's shared memory behind one
+  // cluster barrier; the writers need not outlive it) ----
   const float invS = 1.0f / (float)S;
-  if (CS == 1) {
+  if (CS > 1) cluster_wait();  // pairs with the arrive at kernel start: every CTA of the cluster has started
+  for (int t = tid; t < sp.nsb_local * D; t += kFastThreads) {
+    const int sl = t / D, d = t - sl * D;
+    float s = 0.f;
+    for (int k = 0; k < 8 && 8 * sl + k < sp.nbl; ++k) s += sm.sBlk[(size_t)(8 * sl + k) * D + d];
+    float* dst = sm.sRecv + (size_t)(sp.sb_lo + sl) * D + d;
+    if (rank != 0) st_cluster_f32(cluster_map_u32(smem_u32(dst), 0), s);
+    else *dst = s;
+  }
+  if (CS > 1) cluster_barrier();
+  else __syncthreads();
+  if (rank == 0)
     for (int d = tid; d < D; d += kFastThreads) {
       float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += sm.sRed[w * D + d];
+      for (int k = 0; k < sp.nsb; ++k) s += sm.sRecv[(size_t)k * D + d];
       store_out<T, D>(p, bh, d, s * invS);
     }
-  } else {
-    // ranks 1..CS-1 store their partial into rank 0's shared memory; ONE cluster barrier (release /
-    // acquire) publishes them -- the writers need not outlive it, rank 0 sums in rank order.  (A remote
-    // mbarrier arrival per element instead of the barrier measured the same, 0.7-0.8 us, but racecheck
-    // cannot see that rank 0 outlives the remote stores.)
-    cluster_wait();  // pairs with the arrive at kernel start: every CTA of the cluster has started
-    for (int d = tid; d < D; d += kFastThreads) {
-      float s = 0.f;
-#pragma unroll
-      for (int w = 0; w < NW; ++w) s += sm.sRed[w * D + d];
-      if (rank != 0) st_cluster_f32(cluster_map_u32(smem_u32(sm.sRecv + rank * D + d), 0), s);
-      else sm.sRecv[d] = s;
-    }
-    cluster_barrier();
-    if (rank == 0)
-      for (int d = tid; d < D; d += kFastThreads) {
-        float s = sm.sRecv[d];
-        for (int r = 1; r < CS; ++r) s += sm.sRecv[r * D + d];
-        store_out<T, D>(p, bh, d, s * invS);
-      }
-  }
   FAST_TRACE(8);
 }
 
@@ -432,17 +452,15 @@ __global__ void __launch_bounds__(kFastThreads, kFastThreads == 128 ? 5 : 1) sam
   const int h = blockIdx.x / CS, b = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int S = p.S;
-  const int m_lo = (int)((long long)S * rank / CS), m_hi = (int)((long long)S * (rank + 1) / CS);
-  const int Sl = m_hi - m_lo;
-  const int nj = Sl > warp ? (Sl - warp + NW - 1) / NW : 0;
+  const FastSplit sp(S, rank, CS);
   __shared__ float sWm[NW];
   __shared__ double sWt[NW];
   __shared__ int sWl[NW];
   FastSmem sm;
   sm.sLoc = reinterpret_cast<double*>(smem_raw);
   sm.sE = reinterpret_cast<float*>(sm.sLoc + p.Cmax);
-  sm.sRed = sm.sE + ((p.Cmax + 3) & ~3);
-  sm.sRecv = sm.sRed + NW * D;
+  sm.sBlk = sm.sE + ((p.Cmax + 3) & ~3);
+  sm.sRecv = sm.sBlk + (size_t)((64 * ((sp.nsb + CS - 1) / CS)) / 8) * D;
   sm.sWm = sWm;
   sm.sWt = sWt;
   sm.sWl = sWl;
@@ -452,7 +470,10 @@ __global__ void __launch_bounds__(kFastThreads, kFastThreads == 128 ? 5 : 1) sam
   // ---- a4: thresholds of the warp's first 32 samples (lane per sample), before the wait ----
   const PhiloxStream ps(p.seed, p.offset, kTagValueSampler, (uint32_t)(p.head_offset + h), (uint32_t)(p.batch_offset + b));
   double T0 = 0.0;
-  if (lane < nj) T0 = sample_threshold(p.mode, m_lo + warp + NW * lane, S, ps);
+  {
+    const int m0 = sp.stratum(warp, 0, lane);
+    if (m0 >= 0) T0 = sample_threshold(p.mode, m0, S, ps);
+  }
   FAST_TRACE(1);
   pdl_wait_primary();
   fast_body<T, D, G>(p, sm, CS, rank, T0);

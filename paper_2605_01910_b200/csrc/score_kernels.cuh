@@ -45,9 +45,13 @@ struct ScoreParams {
   int stash_stride;         // Cmax * L
   uint32_t* tickets;        // [B * Hkv], zeroed here for the sample kernel
   uint32_t* flags;          // zeroed here
-  // fused KV append (santa_decode_attention_append; NULL = none): the new token's rows
-  // k_new / v_new [B, Hkv, D] are written into K_w / V_w (the caches K / V, writable) at slot
-  // seqlens[b] - 1 by the producer lane that streams that slot's stage, before its TMA load
+};
+
+// fused KV append (santa_decode_attention_append): the new token's rows k_new / v_new [B, Hkv, D]
+// are written into K_w / V_w (the caches K / V, writable) at slot seqlens[b] - 1 by the producer lane
+// that streams that slot's stage, before its TMA load.  A separate kernel parameter of its own entry
+// point (score_stream_append_kernel), so the plain pass keeps its parameter block.
+struct AppendParams {
   const void* k_new;
   const void* v_new;
   void* K_w;
@@ -269,9 +273,11 @@ struct ChunkWalk {
 // lane keeps one cursor per warp and, polling every warp's next slot with a non-blocking
 // mbarrier.test_wait, issues the next stage for whichever warp has a free slot -- no
 // head-of-line blocking behind a slow warp.
-template <typename T, int D, int G, int NW, int SPW, int kAblate = 0>  // kAblate: tools/microbench_score only
+template <typename T, int D, int G, int NW, int SPW, int kAblate = 0,  // kAblate: tools/microbench_score only
+          bool kAppend = false>  // the fused KV append (santa_decode_attention_append) -- its own instantiation:
+                                 // a runtime test in the producer loop cost the plain pass 1.6 us (14.8 -> 16.4)
 __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const ScoreParams& p,
-                                                  unsigned char* smem_raw) {
+                                                  unsigned char* smem_raw, const AppendParams* ap = nullptr) {
   const CUtensorMap& tmK = *tmKp;
   constexpr int NSLOT = NW * SPW;
   constexpr int kBoxBytes = 64 * 128;
@@ -350,16 +356,16 @@ __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const
           } else {
             row = cw[j].unit * p.kv.page_size + t;  // contiguous [B*Hkv][max_seqlen] rows
           }
-          if (p.k_new) {  // fused append: the new token lands in this stage -> write it first
+          if constexpr (kAppend) {  // fused append: the new token lands in this stage -> write it first
             const int b = cw[j].unit / p.Hkv;
             const int tnew = __ldg(p.seqlens + b) - 1;
             if (tnew >= t && tnew < t + kStageKeys) {
               const int64_t drow = (int64_t)row + (tnew - t);  // cache row of the new token (pages hold
               const int64_t srow = cw[j].unit;                 // whole 64-key stages: same page)
-              const uint4* ks = reinterpret_cast<const uint4*>(p.k_new) + srow * (D * sizeof(T) / 16);
-              const uint4* vs = reinterpret_cast<const uint4*>(p.v_new) + srow * (D * sizeof(T) / 16);
-              uint4* kd = reinterpret_cast<uint4*>(p.K_w) + drow * (D * sizeof(T) / 16);
-              uint4* vd = reinterpret_cast<uint4*>(p.V_w) + drow * (D * sizeof(T) / 16);
+              const uint4* ks = reinterpret_cast<const uint4*>(ap->k_new) + srow * (D * sizeof(T) / 16);
+              const uint4* vs = reinterpret_cast<const uint4*>(ap->v_new) + srow * (D * sizeof(T) / 16);
+              uint4* kd = reinterpret_cast<uint4*>(ap->K_w) + drow * (D * sizeof(T) / 16);
+              uint4* vd = reinterpret_cast<uint4*>(ap->V_w) + drow * (D * sizeof(T) / 16);
 #pragma unroll
               for (int i = 0; i < (int)(D * sizeof(T) / 16); ++i) {
                 kd[i] = __ldg(ks + i);
@@ -488,6 +494,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     score_stream_kernel(const __grid_constant__ CUtensorMap tmK, ScoreParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   score_stream_body<T, D, G, NW, SPW, kAblate>(&tmK, p, smem_raw);
+}
+
+template <typename T, int D, int G, int NW, int SPW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    score_stream_append_kernel(const __grid_constant__ CUtensorMap tmK, ScoreParams p, AppendParams ap) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  score_stream_body<T, D, G, NW, SPW, 0, true>(&tmK, p, smem_raw, &ap);
 }
 
 // ---------------------------------------------------------------------------------------

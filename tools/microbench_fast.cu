@@ -103,7 +103,7 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(skern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
   auto pkern = sample_fast_kernel<bf16, 128, 4>;
   auto launch_pdl = [&](SampleParams p) {
-    const size_t psm = sample_fast_smem_bytes(Cmax, D, p.cluster);
+    const size_t psm = sample_fast_smem_bytes(Cmax, D, p.cluster, S);
     cudaFuncSetAttribute(pkern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(H * p.cluster, B);
