@@ -66,6 +66,8 @@ def parse():
                     help="process-group backend for N > 1 (gloo + --share-gpu: exercise the multi-rank legs "
                          "on one GPU; never a bench number)")
     ap.add_argument("--share-gpu", action="store_true", help="every rank on cuda:0 (test mode, with gloo)")
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE config whose leg to print alone (2 = the default headline line)")
     return ap.parse_args()
 
 
@@ -382,6 +384,27 @@ def config4(args, dev, stream, timed_loop, peak):
     return rows
 
 
+def config1(args, dev, stream, timed_loop, peak):
+    """BASELINE config 1: one head, n_k = 1024, d = 64, fp32, S = 16 systematic, batch 1 -- launch-bound
+    (its purpose is the CPU oracle in seconds and fp32 parity); no roofline claim."""
+    import torch
+
+    import paper_2605_01910_b200 as santa
+    import santa_inputs as si
+
+    inp = si.make_decode_inputs(1, 1, 1, 64, 1024, dtype="f32", seed=1, device=str(dev))
+    geo = santa.make_geometry(inp.q, 1, 1024)
+    ws = santa.workspace(geo, 16, dev)
+    out = torch.empty_like(inp.q)
+    fn = lambda i: santa.santa_decode_attention(geo, inp.q, inp.K, inp.V, inp.seqlens, 16, "systematic",  # noqa
+                                                args.seed, i, out, None, ws, stream)
+    for i in range(10):
+        fn(i)
+    t = timed_loop(fn, max(10, min(args.steps, 200)))
+    return {"us": round(t * 1e3, 2), "path": santa.santa_auto_path(geo, 16),
+            "note": "1 head x 1024 keys x d=64 fp32, S=16 systematic: launch-bound, no roofline claim"}
+
+
 def config5(args, dev, stream, timed_loop, peak):
     """BASELINE config 5: Bernoulli ternary-q score stage (mean-group, stratified, B=8) + the
     S^2ANTA value stage (S=256 stratified), 32k context, batch 16, feature-major K^T; calibrated
@@ -627,6 +650,23 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    if args.config != 2:  # one BASELINE config's leg alone, as its own JSON line
+        peak, peak_src = load_peaks()
+        legs = {1: lambda: config1(args, dev, stream, timed_loop, peak),
+                3: lambda: config3(args, dev, stream, timed_loop, max_over_ranks, peak, world),
+                4: lambda: (config4(args, dev, stream, timed_loop, peak) if world == 1 else
+                            config4_seqshard(args, dev, stream, timed_loop, max_over_ranks, peak, world, rank)),
+                5: lambda: config5(args, dev, stream, timed_loop, peak)}
+        with ClockSampler(local) as clk:
+            leg = legs[args.config]()
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "config": {"baseline_config": args.config}, "n_gpus": world,
+                              "result": leg, "peak_GBps": peak, "peak_source": peak_src, "clocks": clk.summary()}),
+                  flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()

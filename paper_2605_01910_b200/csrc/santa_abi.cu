@@ -12,10 +12,18 @@
 
 #include "host.cuh"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges are no-ops unless a tool (nsys, ncu) attaches
+
 using namespace santa;
 using namespace santa_host;
 
 namespace {
+
+// one NVTX range per public entry point (a profiler timeline shows every ABI call by name)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 
 // idx row length of the flash path: max over sequence lengths <= max_seqlen of S_tile * T
@@ -253,6 +261,7 @@ santa_status santa_decode_attention(const santa_geometry* g, const void* q, cons
                                     const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
                                     uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
                                     void* stream) {
+  NvtxRange nvtx_("santa_decode_attention");
   return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr, stream);
 }
 
@@ -260,6 +269,7 @@ santa_status santa_decode_attention_path(const santa_geometry* g, const void* q,
                                          const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
                                          uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
                                          int32_t path, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_path");
   return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, nullptr, stream,
                        path);
 }
@@ -268,12 +278,14 @@ santa_status santa_decode_attention_profiled(const santa_geometry* g, const void
                                              const void* V, const int32_t* seqlens, int32_t S, int32_t mode,
                                              uint64_t seed, uint64_t offset, void* out, int32_t* idx_out,
                                              void* ws, size_t ws_bytes, void* const* events, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_profiled");
   if (!events || !events[0] || !events[1] || !events[2]) return SANTA_ERR_INVALID_ARG;
   return decode_common(g, q, K, V, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, events, stream);
 }
 
 santa_status santa_score_phase(const santa_geometry* g, const void* q, const void* K, const int32_t* seqlens,
                                void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_score_phase");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (!q || !K || !seqlens) return SANTA_ERR_INVALID_ARG;
@@ -290,6 +302,7 @@ santa_status santa_score_phase(const santa_geometry* g, const void* q, const voi
 santa_status santa_sample_phase(const santa_geometry* g, const void* V, const int32_t* seqlens, int32_t S,
                                 int32_t mode, uint64_t seed, uint64_t offset, void* out, int32_t* idx_out, void* ws,
                                 size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_sample_phase");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
@@ -310,6 +323,7 @@ santa_status santa_sample_phase(const santa_geometry* g, const void* V, const in
 santa_status santa_decode_attention_prop(const santa_geometry* g, const void* q, const void* K, const void* V,
                                          const int32_t* seqlens, int32_t S, uint64_t seed, uint64_t offset,
                                          void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_prop");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
@@ -336,6 +350,7 @@ santa_status santa_decode_attention_flash(const santa_geometry* g, const void* q
                                           const int32_t* seqlens, int32_t S, int32_t tile_len, uint64_t seed,
                                           uint64_t offset, void* out, int32_t* idx_out, void* ws, size_t ws_bytes,
                                           void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_flash");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
@@ -364,6 +379,7 @@ int32_t santa_flash_max_samples(const santa_geometry* g, int32_t S, int32_t tile
 
 santa_status santa_dense_reference(const santa_geometry* g, const void* q, const void* K, const void* V,
                                    const int32_t* seqlens, void* out, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_dense_reference");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if ((s = validate_decode_ptrs(q, K, V, seqlens, out)) != SANTA_OK) return s;
@@ -380,6 +396,7 @@ santa_status santa_bernoulli_scores(const santa_geometry* g, const void* q, cons
                                     int32_t nB, int32_t stratified, int32_t mean_group, uint64_t seed,
                                     uint64_t offset, float* scores, uint8_t* feature_mask, void* ws,
                                     size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_bernoulli_scores");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if ((s = validate_bern(g, q, Kt, seqlens, nB)) != SANTA_OK) return s;
@@ -401,6 +418,7 @@ santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const voi
                                               int32_t mean_group, int32_t S, int32_t mode, uint64_t seed,
                                               uint64_t offset, void* out, int32_t* idx_out, void* ws,
                                               size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_bernoulli");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if ((s = validate_bern(g, q, Kt, seqlens, nB)) != SANTA_OK) return s;
@@ -428,6 +446,7 @@ santa_status santa_decode_attention_bernoulli(const santa_geometry* g, const voi
 santa_status santa_seqshard_stats(const santa_geometry* g, const void* q, const void* K_shard,
                                   const int32_t* shard_seqlens, double* stats_out, void* ws, size_t ws_bytes,
                                   void* stream) {
+  NvtxRange nvtx_("santa_seqshard_stats");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (!q || !K_shard || !shard_seqlens || !stats_out) return SANTA_ERR_INVALID_ARG;
@@ -450,6 +469,7 @@ santa_status santa_seqshard_sample_gather(const santa_geometry* g, const double*
                                           const int32_t* shard_seqlens, int32_t S, int32_t mode, uint64_t seed,
                                           uint64_t offset, float* partial_out, int32_t* idx_out, void* ws,
                                           size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_seqshard_sample_gather");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (S < 1) return SANTA_ERR_EMPTY_BUDGET;
@@ -475,6 +495,7 @@ santa_status santa_decode_step_host(const santa_geometry* g, const void* q_host,
                                     void* K, void* V, const int32_t* seqlens, int32_t S, int32_t mode,
                                     uint64_t seed, uint64_t offset, void* out_dev, void* out_host, void* ws,
                                     size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_decode_step_host");
   if (!q_host || !k_new_host || !v_new_host || !q_dev || !k_new_dev || !v_new_dev || !out_host)
     return SANTA_ERR_INVALID_ARG;
   // the whole decode validation runs before the first copy (nothing is touched on error)
@@ -501,6 +522,7 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
                                            void* V, const int32_t* seqlens, int32_t S, int32_t mode, uint64_t seed,
                                            uint64_t offset, void* out_dev, void* out_host, void* ws, size_t ws_bytes,
                                            int32_t synchronize, void* stream) {
+  NvtxRange nvtx_("santa_decode_step_host_packed");
   santa_status s = validate_geometry(g);
   if (s != SANTA_OK) return s;
   if (!qkv_host || !qkv_dev || !out_host) return SANTA_ERR_INVALID_ARG;
@@ -569,6 +591,7 @@ santa_status santa_decode_attention_append(const santa_geometry* g, const void* 
                                            const void* k_new, const void* v_new, const int32_t* seqlens, int32_t S,
                                            int32_t mode, uint64_t seed, uint64_t offset, void* out,
                                            int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_append");
   return decode_append(g, q, K, V, k_new, v_new, seqlens, S, mode, seed, offset, out, idx_out, ws, ws_bytes, stream);
 }
 
@@ -592,6 +615,7 @@ santa_status santa_decode_attention_layer(const santa_geometry* g, const santa_l
                                           const void* q, void* K, void* V, const void* k_new, const void* v_new,
                                           const int32_t* seqlens, int32_t mode, uint64_t seed, uint64_t offset,
                                           void* out, int32_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nvtx_("santa_decode_attention_layer");
   santa_status s = check_schedule(sched);
   if (s != SANTA_OK) return s;
   if (layer < 0 || layer >= sched->n_layers) return SANTA_ERR_INVALID_ARG;
