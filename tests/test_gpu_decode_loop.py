@@ -110,3 +110,37 @@ def test_per_layer_schedule():
     with pytest.raises(santa.SantaError):
         santa.santa_decode_attention_layer(geo, sched, 4, inp.q, inp.K, inp.V, None, None, inp.seqlens,
                                            "stratified", 9, step, out, idx, ws)
+
+
+def test_prepared_decode_equals_the_plain_call():
+    """prepare_decode (arguments marshalled once, launch(offset) per step) launches exactly the
+    santa_decode_attention_path call: same bits for every offset."""
+    inp = to_cuda(si.make_decode_inputs(2, 32, 8, 128, [4000, 2500], dtype="bf16", seed=76))
+    geo = santa.make_geometry(inp.q, 8, inp.K.shape[2])
+    ws = santa.workspace(geo, 128)
+    out = torch.empty_like(inp.q)
+    idx = torch.empty(2, 32, 128, dtype=torch.int32, device="cuda")
+    launch = santa.prepare_decode(geo, inp.q, inp.K, inp.V, inp.seqlens, 128, "systematic", 4, out, idx, ws)
+    for off in (0, 5, 123456789):
+        launch(off)
+        ref_out, ref_idx = santa.decode(inp.q, inp.K, inp.V, inp.seqlens, 128, "systematic", 4, off, return_idx=True)
+        torch.cuda.synchronize()
+        assert torch.equal(idx, ref_idx) and torch.equal(out, ref_out), off
+
+
+@pytest.mark.parametrize("dtype,d,H,Hkv", [("f16", 64, 16, 2), ("bf16", 128, 8, 8)])
+def test_append_dtype_shape_variants(dtype, d, H, Hkv):
+    """The fused append on fp16 / d = 64 / G = 8 and on G = 1 geometries."""
+    n = [1700, 900]
+    inp = to_cuda(si.make_decode_inputs(2, H, Hkv, d, n, dtype=dtype, seed=77))
+    k_new, v_new = _new_rows(2, Hkv, d, inp.K.dtype, 78)
+    K_ref, V_ref = inp.K.clone(), inp.V.clone()
+    for b, nb in enumerate(n):
+        K_ref[b, :, nb - 1] = k_new[b]
+        V_ref[b, :, nb - 1] = v_new[b]
+    out_ref, idx_ref = santa.decode(inp.q, K_ref, V_ref, inp.seqlens, 64, "stratified", 8, 0, return_idx=True)
+    K, V = inp.K.clone(), inp.V.clone()
+    out, idx = santa.decode_append(inp.q, K, V, k_new, v_new, inp.seqlens, 64, "stratified", 8, 0, return_idx=True)
+    torch.cuda.synchronize()
+    assert torch.equal(K, K_ref) and torch.equal(V, V_ref)
+    assert torch.equal(idx, idx_ref) and torch.equal(out, out_ref)
