@@ -47,7 +47,19 @@ struct BernParams {
   int sub64;                // 1: stats/stash per 64-key sub-chunk (Cmax/stash_stride of the L = 64 layout)
   uint32_t* tickets;
   uint32_t* flags;
+  uint2* wfrag;             // [B*Hkv][D/16][3][32] bf16-part B fragments (bern_tma_kernel) or NULL
 };
+
+// B-fragment value of one bf16 part (0 = hi, 1 = mid, 2 = lo) of an fp32 weight: w = hi + mid + lo
+// to 2^-24 |w| (bern_tma_kernel.cuh)
+__device__ __forceinline__ uint16_t bern_weight_part(float w, int part) {
+  __nv_bfloat16 h = __float2bfloat16_rn(w);
+  if (part == 0) return __bfloat16_as_ushort(h);
+  const float r1 = w - __bfloat162float(h);  // exact
+  h = __float2bfloat16_rn(r1);
+  if (part == 1) return __bfloat16_as_ushort(h);
+  return __bfloat16_as_ushort(__float2bfloat16_rn(r1 - __bfloat162float(h)));
+}
 
 template <typename T, int D, int G>
 __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
@@ -124,6 +136,25 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
     int tot = 0;
     for (int k = 0; k < D / 32; ++k) tot += sWarpCnt[k];
     p.sel_n[unit] = tot;
+  }
+  if (p.wfrag != nullptr) {
+    // m16n8k16 B fragments of the weights in selection order (bern_tma_kernel): group kg of 16
+    // selected features, part q of the 3-way bf16 split, lane (g, t) = (head g, features 2t, 2t+1
+    // and 2t+8, 2t+9); heads >= G and features past |F| are 0.  The sel / w stores above are
+    // visible to the block after the barrier.
+    __syncthreads();
+    int nsel = 0;
+    for (int k = 0; k < D / 32; ++k) nsel += sWarpCnt[k];
+    const int* sel = p.sel + unit * D;
+    uint2* wf = p.wfrag + unit * (D / 16) * 96;
+    for (int e = i; e < (D / 16) * 96; e += D) {
+      const int kg = e / 96, q = (e / 32) % 3, ln = e % 32;
+      const int g = ln >> 2, s0 = 16 * kg + 2 * (ln & 3);
+      auto part = [&](int s) -> uint32_t {
+        return (g < G && s < nsel) ? (uint32_t)bern_weight_part(w[g * D + sel[s]], q) : 0u;
+      };
+      wf[e] = make_uint2(part(s0) | (part(s0 + 1) << 16), part(s0 + 8) | (part(s0 + 9) << 16));
+    }
   }
 }
 

@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include "bernoulli_kernels.cuh"
+#include "bern_tma_kernel.cuh"
 #include "common.cuh"
 #include "dense_kernels.cuh"
 #include "dense_stream_kernel.cuh"
@@ -43,7 +44,7 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 struct WsLayout {
   int L = 64, Cmax = 0, Cmax256 = 0;
-  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, sync = 0, bern = 0, total = 0;
+  size_t stash = 0, cstats = 0, tickets = 0, flags = 0, sync = 0, bern = 0, bfrag = 0, total = 0;
   size_t step_rec = 0, step_stash = 0, step_part = 0;  // step kernel's tagged regions
   size_t dense_o = 0, dense_ml = 0;  // dense_split_kernel partials
 };
@@ -96,6 +97,7 @@ inline WsLayout layout(const santa_geometry* g, int S) {
   const size_t cmx = L.Cmax > L.Cmax256 ? L.Cmax : L.Cmax256;
   L.cstats = off; off = align256(off + B * H * cmx * 8);
   L.bern = off; off = align256(off + B * Hkv * ((size_t)G * D * 4 + D * 4 + 256));  // weights, sel, sel_n
+  L.bfrag = off; off = align256(off + B * Hkv * (size_t)(D / 16) * 96 * 8);  // bern_tma_kernel B fragments
   // step kernel: tagged chunk records, tagged fixed-point stash, tagged split partials (separate
   // from the two-kernel path's untagged regions so the paths can share one workspace)
   L.step_rec = off; off = align256(off + B * H * (size_t)L.Cmax * 16);

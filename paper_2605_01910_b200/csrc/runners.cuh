@@ -358,9 +358,33 @@ santa_status RunBern<T, D, G>::run(const DecodeArgs& a, const void* Kt, int nB, 
   p.stash_stride = p.sub64 ? a.L.Cmax * 64 : a.L.Cmax256 * kDenseChunk;
   p.tickets = at<uint32_t>(a.ws, a.L.tickets);
   p.flags = at<uint32_t>(a.ws, a.L.flags);
+  // bf16 decode on 64-key chunks with 16-B aligned feature rows: the TMA + tensor-core stream
+  // (bern_tma_kernel.cuh); its B fragments are built by the weights kernel
+  static const bool force_fma = std::getenv("SANTA_BERN_FMA") != nullptr;  // A/B switch (tools)
+  bool tma = false;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const int P = a.g->page_table ? a.g->page_size : a.g->max_seqlen;
+    tma = for_decode && p.sub64 && scores == nullptr && P % 8 == 0 && (reinterpret_cast<uintptr_t>(Kt) & 15) == 0 &&
+          (a.g->page_table == nullptr || P % kBtKeys == 0 || (P >= kBtMinPage && kBtKeys % P == 0)) &&
+          !force_fma;
+  }
+  p.wfrag = tma ? at<uint2>(a.ws, a.L.bfrag) : nullptr;
   if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
       cudaSuccess)
     return SANTA_ERR_CUDA;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (tma) {
+      const int nblk = (a.g->max_seqlen + kBtKeys - 1) / kBtKeys;
+      const int items = a.g->batch * a.g->n_kv_heads * nblk;
+      const int grid = std::min(items, num_sms());
+      const size_t smem = bern_tma_smem_bytes(G);
+      if (ensure_smem(bern_tma_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+      if (launch(bern_tma_kernel<T, D, G>, dim3(grid), dim3(32 * (kBtWarps + kBtProducers)), smem, a.st, true, p, items) !=
+          cudaSuccess)
+        return SANTA_ERR_CUDA;
+      return SANTA_OK;
+    }
+  }
   if constexpr (sizeof(T) == 2) {
     if (for_decode && p.sub64) {  // decode on 64-key chunks: the persistent stream (bern_stream_kernel)
       const int nblk = (a.g->max_seqlen + kBernBlockKeys - 1) / kBernBlockKeys;
