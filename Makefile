@@ -18,11 +18,15 @@ T_bf16 := __nv_bfloat16
 T_f16 := __half
 T_f32 := float
 INST_OBJS := $(foreach f,$(FAMS),$(foreach t,$(DTS),$(foreach d,$(DS),$(OBJDIR)/inst_$(f)_$(t)_$(d).o)))
-OBJS := $(OBJDIR)/santa_abi.o $(INST_OBJS)
+OBJS := $(OBJDIR)/santa_abi.o $(OBJDIR)/peer_exchange.o $(INST_OBJS)
 
 all: $(LIB)
 
 $(OBJDIR)/santa_abi.o: $(CSRC)/santa_abi.cu $(HDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.log || (cat $@.log; exit 1)
+
+$(OBJDIR)/peer_exchange.o: $(CSRC)/peer_exchange.cu include/santa.h
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> $@.log || (cat $@.log; exit 1)
 
@@ -35,7 +39,7 @@ $(OBJDIR)/inst_%.o: $(CSRC)/inst.cu $(HDR)
 $(LIB): $(OBJS)
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
-	@cat $(OBJDIR)/santa_abi.o.log $(INST_OBJS:=.log) > $(LIBDIR)/ptxas.log
+	@cat $(OBJDIR)/santa_abi.o.log $(OBJDIR)/peer_exchange.o.log $(INST_OBJS:=.log) > $(LIBDIR)/ptxas.log
 
 sass: $(LIB)
 	cuobjdump -sass $(LIB) > $(LIBDIR)/libsanta.sass

@@ -78,6 +78,8 @@ typedef enum { SANTA_BF16 = 0, SANTA_F32 = 1, SANTA_F16 = 2 } santa_dtype; /* q,
 #define SANTA_FLAG_SYNC_TIMEOUT 0x100u  /* the single-launch step kernel gave up waiting (~0.5 s)  */
                                         /* on a unit counter: the workspace was not zero at rest   */
                                         /* (see santa_workspace_bytes); outputs are invalid        */
+#define SANTA_FLAG_PEER_TIMEOUT 0x200u  /* a peer exchange gave up waiting for a rank (2 s): some   */
+                                        /* rank did not make the same call; its outputs are invalid */
 
 typedef enum {
   SANTA_PATH_AUTO = 0,        /* santa_auto_path's choice                                         */
@@ -378,6 +380,61 @@ santa_status santa_philox_uniforms(uint64_t seed, uint64_t offset, int32_t tag, 
 
 /* Reads (and clears) the workspace flag word: syncs `stream`, copies it to *flags_out. */
 santa_status santa_read_error_flags(void* workspace, uint32_t* flags_out, void* stream);
+
+/* Peer-memory exchange for the sequence-sharded step (config 4).
+ *
+ * The two collectives of santa_seqshard_* -- the all-gather of every rank's [B, H, 2] fp64
+ * (m_r, L_r) and the SUM of the [B, H, d] fp32 partial outputs (reading #18; the exchange is an
+ * extension, no paper passage) -- as ONE kernel each over NVLink peer memory: every rank stores
+ * its payload into slot `rank` of every rank's exchange buffer (P2P stores through CUDA-IPC
+ * mappings), releases a per-(source, block) flag there, acquires the flags of all sources in its
+ * own buffer and consumes its slots.  The SUM adds the slots in rank order 0..world-1 in fp32,
+ * so every rank gets bit-identical results.
+ *
+ * group->bufs[r] is rank r's exchange buffer as addressable from THIS process (its own
+ * allocation for r == rank, a santa_ipc_import mapping otherwise), every one 256-B aligned and
+ * group->buf_bytes long (>= santa_peer_buffer_bytes(world, largest payload)), zeroed by the
+ * caller once before the first call (flag word at offset 0 readable with santa_read_error_flags).
+ * `epoch` numbers the calls on the group: 1, 2, 3, ... (+1 per call, all ranks the same sequence
+ * of calls); call e uses buffer half e & 1.
+ *
+ * n_local ranks are served by one launch: ranks[l], src[l], dst[l] (host arrays of device
+ * pointers) for l < n_local.  A multi-GPU run passes n_local = 1 (its own rank).  n_local = world
+ * emulates the whole group in ONE cooperative launch on one GPU (every rank's buffer allocated on
+ * it) -- the test configuration; separate per-rank launches that wait on each other on one GPU
+ * are not supported.  A wait that sees no flag for 2 s gives up and sets SANTA_FLAG_PEER_TIMEOUT in
+ * the own buffer's flag word (never a hang).
+ *
+ * allgather: src[l] = `bytes` (multiple of 16) of payload; dst[l] = [world][bytes].
+ * allreduce_f32: src[l], dst[l] = `count` fp32 (count * 4 a multiple of 16); dst may equal src.
+ * Errors: SANTA_ERR_INVALID_ARG (NULL, world not in 1..8, ranks repeated / out of range,
+ * epoch 0), SANTA_ERR_ALIGNMENT, SANTA_ERR_WORKSPACE (payload larger than a slot),
+ * SANTA_ERR_CUDA (launch refused). */
+typedef struct {
+  int32_t world;      /* ranks in the group, 1..8 */
+  void* bufs[8];      /* bufs[r]: rank r's exchange buffer, mapped into this process */
+  size_t buf_bytes;   /* bytes of every rank's buffer */
+} santa_peer_group;
+
+#define SANTA_IPC_HANDLE_BYTES 64
+
+/* Buffer bytes for payloads of up to max_payload_bytes per rank (0 if world not in 1..8). */
+size_t santa_peer_buffer_bytes(int32_t world, size_t max_payload_bytes);
+santa_status santa_peer_allgather(const santa_peer_group* group, int32_t n_local, const int32_t* ranks,
+                                  const void* const* src, void* const* dst, size_t bytes, uint32_t epoch,
+                                  void* stream);
+santa_status santa_peer_allreduce_f32(const santa_peer_group* group, int32_t n_local, const int32_t* ranks,
+                                      const float* const* src, float* const* dst, size_t count, uint32_t epoch,
+                                      void* stream);
+
+/* CUDA-IPC plumbing for the exchange buffers (host only, no kernel): santa_ipc_export writes the
+ * 64-B handle of the allocation holding dev_ptr and dev_ptr's offset in it; santa_ipc_import (in
+ * another process) maps it and returns the peer's dev_ptr (base + offset) and the mapping base,
+ * which santa_ipc_close unmaps.  An allocation cannot be imported into the process that exported
+ * it (pass the own pointer instead). */
+santa_status santa_ipc_export(const void* dev_ptr, void* handle_out, size_t* offset_out);
+santa_status santa_ipc_import(const void* handle, size_t offset, void** dev_ptr_out, void** base_out);
+santa_status santa_ipc_close(void* base);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

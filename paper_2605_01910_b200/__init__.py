@@ -16,7 +16,8 @@ from typing import Optional, Sequence
 import torch
 
 from . import _abi
-from ._abi import DTYPES, FLAG_EMPTY_SEQ, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry, LayerSchedule, SantaError
+from ._abi import (DTYPES, FLAG_EMPTY_SEQ, FLAG_PEER_TIMEOUT, FLAG_SYNC_TIMEOUT, MODES, PATHS, Geometry,
+                   LayerSchedule, PeerGroup, SantaError)
 
 __all__ = [
     "Geometry", "SantaError", "MODES", "make_geometry", "workspace", "santa_workspace_bytes", "santa_auto_path",
@@ -29,6 +30,8 @@ __all__ = [
     "santa_read_error_flags", "santa_version", "decode", "decode_prop", "dense", "LIB_PATH",
     "santa_decode_attention_append", "LayerSchedule", "make_schedule", "santa_schedule_workspace_bytes",
     "santa_decode_attention_layer", "decode_append", "prepare_decode",
+    "PeerGroup", "FLAG_PEER_TIMEOUT", "make_peer_group", "santa_peer_buffer_bytes", "santa_peer_allgather",
+    "santa_peer_allreduce_f32", "santa_ipc_export", "santa_ipc_import", "santa_ipc_close",
 ]
 LIB_PATH = _abi.LIB_PATH
 _TORCH_DT = {torch.bfloat16: "bf16", torch.float32: "f32", torch.float16: "f16"}
@@ -275,6 +278,68 @@ def santa_read_error_flags(ws, stream=None) -> int:
     f = ctypes.c_uint32(0)
     _abi.check("santa_read_error_flags", _abi.LIB.santa_read_error_flags(_ptr(ws), ctypes.byref(f), _stream(stream)))
     return int(f.value)
+
+
+def santa_peer_buffer_bytes(world: int, max_payload_bytes: int) -> int:
+    return int(_abi.LIB.santa_peer_buffer_bytes(world, max_payload_bytes))
+
+
+def make_peer_group(bufs: Sequence[int], buf_bytes: int) -> PeerGroup:
+    """santa_peer_group from every rank's buffer address (ints, as mapped into this process)."""
+    g = PeerGroup()
+    g.world = len(bufs)
+    for r, p in enumerate(bufs):
+        g.bufs[r] = int(p)
+    g.buf_bytes = int(buf_bytes)
+    return g
+
+
+def _ptr_array(ptrs, ctype=ctypes.c_void_p):
+    return (ctype * len(ptrs))(*ptrs)
+
+
+def santa_peer_allgather(group: PeerGroup, ranks: Sequence[int], src: Sequence[torch.Tensor],
+                         dst: Sequence[torch.Tensor], epoch: int, stream=None):
+    """One-shot all-gather: src[l] (this call's rank ranks[l]) -> dst[l] = [world, *src shape]."""
+    nbytes = src[0].numel() * src[0].element_size()
+    for s_, d_ in zip(src, dst):
+        if s_.numel() * s_.element_size() != nbytes or d_.numel() * d_.element_size() != group.world * nbytes:
+            raise ValueError("allgather: src / dst sizes")
+    _abi.check("santa_peer_allgather", _abi.LIB.santa_peer_allgather(
+        ctypes.byref(group), len(ranks), _ptr_array(ranks, ctypes.c_int32), _ptr_array([_ptr(t) for t in src]),
+        _ptr_array([_ptr(t) for t in dst]), nbytes, epoch, _stream(stream)))
+
+
+def santa_peer_allreduce_f32(group: PeerGroup, ranks: Sequence[int], src: Sequence[torch.Tensor],
+                             dst: Sequence[torch.Tensor], epoch: int, stream=None):
+    """One-shot SUM in rank order: dst[l] = sum_r src of rank r (fp32; dst may be src)."""
+    n = src[0].numel()
+    for s_, d_ in zip(src, dst):
+        if s_.dtype != torch.float32 or d_.dtype != torch.float32 or s_.numel() != n or d_.numel() != n:
+            raise ValueError("allreduce_f32: fp32 tensors of equal size")
+    _abi.check("santa_peer_allreduce_f32", _abi.LIB.santa_peer_allreduce_f32(
+        ctypes.byref(group), len(ranks), _ptr_array(ranks, ctypes.c_int32), _ptr_array([_ptr(t) for t in src]),
+        _ptr_array([_ptr(t) for t in dst]), n, epoch, _stream(stream)))
+
+
+def santa_ipc_export(t: torch.Tensor):
+    """(64-byte handle, offset) of a device tensor's allocation for santa_ipc_import elsewhere."""
+    h = ctypes.create_string_buffer(_abi.IPC_HANDLE_BYTES)
+    off = ctypes.c_size_t(0)
+    _abi.check("santa_ipc_export", _abi.LIB.santa_ipc_export(_ptr(t), h, ctypes.byref(off)))
+    return bytes(h.raw), int(off.value)
+
+
+def santa_ipc_import(handle: bytes, offset: int):
+    """Maps a peer's exported allocation: (device address of the peer tensor, mapping base)."""
+    p, base = ctypes.c_void_p(), ctypes.c_void_p()
+    hb = ctypes.create_string_buffer(bytes(handle), _abi.IPC_HANDLE_BYTES)
+    _abi.check("santa_ipc_import", _abi.LIB.santa_ipc_import(hb, offset, ctypes.byref(p), ctypes.byref(base)))
+    return int(p.value), int(base.value)
+
+
+def santa_ipc_close(base: int):
+    _abi.check("santa_ipc_close", _abi.LIB.santa_ipc_close(ctypes.c_void_p(base)))
 
 
 # ---- convenience wrappers (allocation + the call; still no compute in Python) ----------------

@@ -18,6 +18,8 @@ MODES = {"iid": 0, "stratified": 1, "systematic": 2}
 DTYPES = {"bf16": 0, "f32": 1, "f16": 2}
 FLAG_EMPTY_SEQ = 0x1
 FLAG_SYNC_TIMEOUT = 0x100
+FLAG_PEER_TIMEOUT = 0x200
+IPC_HANDLE_BYTES = 64
 PATHS = {"auto": 0, "step": 1, "two_kernel": 2, "step_tc": 3}
 
 
@@ -46,6 +48,10 @@ class Geometry(ctypes.Structure):
         ("batch_offset", ctypes.c_int32),
         ("head_offset", ctypes.c_int32),
     ]
+
+
+class PeerGroup(ctypes.Structure):
+    _fields_ = [("world", ctypes.c_int32), ("bufs", ctypes.c_void_p * 8), ("buf_bytes", ctypes.c_size_t)]
 
 
 def _load() -> ctypes.CDLL:
@@ -84,6 +90,12 @@ def _load() -> ctypes.CDLL:
         "santa_schedule_workspace_bytes": ([G, ctypes.POINTER(LayerSchedule)], sz),
         "santa_decode_attention_layer": ([G, ctypes.POINTER(LayerSchedule), i32, vp, vp, vp, vp, vp, vp, i32, u64,
                                           u64, vp, vp, vp, sz, vp], i32),
+        "santa_peer_buffer_bytes": ([i32, sz], sz),
+        "santa_peer_allgather": ([ctypes.POINTER(PeerGroup), i32, vp, vp, vp, sz, ctypes.c_uint32, vp], i32),
+        "santa_peer_allreduce_f32": ([ctypes.POINTER(PeerGroup), i32, vp, vp, vp, sz, ctypes.c_uint32, vp], i32),
+        "santa_ipc_export": ([vp, vp, ctypes.POINTER(sz)], i32),
+        "santa_ipc_import": ([vp, sz, ctypes.POINTER(vp), ctypes.POINTER(vp)], i32),
+        "santa_ipc_close": ([vp], i32),
     }
     for name, (args, res) in sigs.items():
         if os.environ.get("SANTA_LIB_PATH") and not hasattr(lib, name):

@@ -13,6 +13,10 @@ torch.distributed for the plumbing).
    the CDF and gathers its local V rows; one all_reduce(SUM) of the [B, H, d] fp32 partials gives
    the output.  The sampled indices equal the unsharded ones (up to boundary rounding).
 
+The two collectives run either through torch.distributed (NCCL) or through ``PeerExchange``: one-shot
+peer-memory kernels of libsanta (santa_peer_allgather / santa_peer_allreduce_f32) that store straight
+into every peer's CUDA-IPC-mapped exchange buffer over NVLink and sum the partials in fixed rank order.
+
 The per-rank compute is a pluggable backend (``CudaBackend`` below = the C-ABI kernels); the
 functions here only move tensors between ranks.  CPU tests drive the same orchestration with
 world_size 2 over gloo and an oracle backend supplied by the test.
@@ -131,13 +135,99 @@ def shard_ranges(seqlens, rank: int, world: int, device=None):
     return lo.to(device) if device is not None else lo, (hi - lo).to(device) if device is not None else hi - lo
 
 
+class PeerExchange:
+    """One-shot peer-memory collectives for one rank per process (n_local = 1): an exchange buffer
+    per rank, exported with CUDA IPC and mapped into every other rank (handles swapped once with
+    all_gather_object over the process group), then each collective is ONE libsanta kernel.
+    ``epoch`` counts the calls; every rank must issue the same sequence of calls."""
+
+    def __init__(self, max_payload_bytes: int, group=None, device=None):
+        from . import make_peer_group, santa_ipc_export, santa_ipc_import, santa_peer_buffer_bytes
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.nbytes = santa_peer_buffer_bytes(self.world, max_payload_bytes)
+        if self.nbytes == 0:
+            raise ValueError("PeerExchange: world must be 1..8")
+        self.max_payload = max_payload_bytes
+        self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
+        torch.cuda.synchronize(self.buf.device)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, santa_ipc_export(self.buf), group=group)
+        self._bases, ptrs = [], []
+        for r, (h, off) in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self.buf.data_ptr())
+            else:
+                p, base = santa_ipc_import(h, off)
+                ptrs.append(p)
+                self._bases.append(base)
+        self.peer_group = make_peer_group(ptrs, self.nbytes)
+        self.epoch = 0
+        dist.barrier(group=group)
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        from . import santa_peer_allgather
+        t = t.contiguous()
+        out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        self.epoch += 1
+        santa_peer_allgather(self.peer_group, [self.rank], [t], [out], self.epoch)
+        return out
+
+    def all_reduce_(self, t: torch.Tensor) -> torch.Tensor:
+        from . import santa_peer_allreduce_f32
+        self.epoch += 1
+        santa_peer_allreduce_f32(self.peer_group, [self.rank], [t], [t], self.epoch)
+        return t
+
+    def close(self):
+        from . import santa_ipc_close
+        torch.cuda.synchronize(self.buf.device)
+        dist.barrier(group=self.group)      # no peer still writes into a mapping we drop
+        for b in self._bases:
+            santa_ipc_close(b)
+        self._bases = []
+
+
+class EmulatedPeerGroup:
+    """All ranks of a group on ONE GPU (tests and single-GPU timing): every rank's exchange buffer
+    is a local allocation and each collective serves all ranks in one cooperative launch
+    (n_local = world) -- the only supported way to run ranks that wait on each other on one GPU."""
+
+    def __init__(self, world: int, max_payload_bytes: int, device="cuda"):
+        from . import make_peer_group, santa_peer_buffer_bytes
+        self.world = world
+        self.nbytes = santa_peer_buffer_bytes(world, max_payload_bytes)
+        if self.nbytes == 0:
+            raise ValueError("EmulatedPeerGroup: world must be 1..8")
+        self.bufs = [torch.zeros(self.nbytes, dtype=torch.uint8, device=device) for _ in range(world)]
+        self.peer_group = make_peer_group([b.data_ptr() for b in self.bufs], self.nbytes)
+        self.epoch = 0
+
+    def all_gather(self, ts):
+        from . import santa_peer_allgather
+        ts = [t.contiguous() for t in ts]
+        outs = [torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device) for t in ts]
+        self.epoch += 1
+        santa_peer_allgather(self.peer_group, list(range(self.world)), ts, outs, self.epoch)
+        return outs
+
+    def all_reduce_(self, ts):
+        from . import santa_peer_allreduce_f32
+        self.epoch += 1
+        santa_peer_allreduce_f32(self.peer_group, list(range(self.world)), ts, ts, self.epoch)
+        return ts
+
+
 def seqshard_decode(q: torch.Tensor, K_shard: torch.Tensor, V_shard: torch.Tensor, seqlens: torch.Tensor,
                     S: int, mode: str, seed: int, offset: int = 0, backend=None, group=None,
-                    return_idx: bool = False, ranges=None):
+                    return_idx: bool = False, ranges=None, exchange: Optional[PeerExchange] = None):
     """Sequence-sharded S^2ANTA decode step (config 4).  Every rank passes its own contiguous
     K/V shard [B, H_kv, n_local, d] and the FULL q [B, H, d] and seqlens [B] (global lengths).
     ``ranges``: this rank's (token_offset, shard_len) from shard_ranges(), precomputed by a decode
     loop (else derived from seqlens here, with a device-to-host read).
+    ``exchange``: a PeerExchange to run both collectives as one-shot peer-memory kernels (else
+    torch.distributed: NCCL all_gather_into_tensor / all_reduce, gloo all_gather / all_reduce).
     Returns the summed output [B, H, d] fp32 on every rank (and this rank's global indices, -1
     for strata owned by other ranks, if return_idx)."""
     backend = backend or CudaBackend()
@@ -150,6 +240,12 @@ def seqshard_decode(q: torch.Tensor, K_shard: torch.Tensor, V_shard: torch.Tenso
             raise ValueError("K_shard too short for this rank's token range")
     lo, shard_len = ranges
     stats = backend.stats(q, K_shard, shard_len, K_shard.shape[1], S)           # [B, H, 2] fp64
+    if exchange is not None:
+        stats_all = exchange.all_gather(stats)                                  # one-shot P2P kernel
+        partial, idx = backend.sample_gather(stats_all, rank, world, lo, V_shard, shard_len, S, mode, seed,
+                                             offset, return_idx=return_idx)
+        exchange.all_reduce_(partial)                                           # fixed rank order
+        return (partial, idx) if return_idx else partial
     stats_all = torch.empty((world,) + tuple(stats.shape), dtype=stats.dtype, device=stats.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(stats_all, stats, group=group)              # the exchange step

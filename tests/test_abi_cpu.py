@@ -177,3 +177,27 @@ def test_layer_schedule_host_logic():
     assert santa.santa_schedule_workspace_bytes(g, santa.make_schedule([8, 0])) == 0       # S < 1
     assert santa.santa_schedule_workspace_bytes(g, santa.make_schedule([8, 5000])) == 0    # S > 4096
     assert santa.santa_schedule_workspace_bytes(_geo(head_dim=96), sched) == 0
+
+
+def test_peer_exchange_host_checks():
+    """santa_peer_* (config 4's one-shot exchange): buffer arithmetic and argument checks need no GPU."""
+    assert santa.santa_peer_buffer_bytes(2, 512) == 8192 + 2 * 2 * 512
+    assert santa.santa_peer_buffer_bytes(8, 100) == 8192 + 2 * 8 * 256     # slots rounded to 256 B
+    assert santa.santa_peer_buffer_bytes(0, 512) == 0
+    assert santa.santa_peer_buffer_bytes(9, 512) == 0
+    g = santa.make_peer_group([0x10000, 0x20000], santa.santa_peer_buffer_bytes(2, 4096))
+    ranks = (ctypes.c_int32 * 2)(0, 1)
+    ptrs = (ctypes.c_void_p * 2)(0x30000, 0x40000)
+    call = lambda **kw: _abi.LIB.santa_peer_allgather(  # noqa: E731
+        ctypes.byref(kw.get("g", g)), kw.get("n", 2), kw.get("ranks", ranks), ptrs, ptrs, kw.get("nb", 4096),
+        kw.get("epoch", 1), None)
+    assert call(epoch=0) == 1                       # INVALID_ARG
+    assert call(n=3) == 1                           # more local ranks than the group
+    assert call(ranks=(ctypes.c_int32 * 2)(1, 1)) == 1
+    assert call(nb=4100) == 7                       # ALIGNMENT: payload not a multiple of 16
+    assert call(nb=8192) == 6                       # WORKSPACE: payload larger than a slot
+    g2 = santa.make_peer_group([0x10000, 0x20010], g.buf_bytes)
+    assert call(g=g2) == 7                          # buffer not 256-B aligned
+    g9 = santa.make_peer_group([0x10000] * 8, g.buf_bytes)
+    g9.world = 9
+    assert call(g=g9) == 1
