@@ -549,9 +549,43 @@ def config4_seqshard(args, dev, stream, timed_loop, max_over_ranks, peak, world,
            "note": ("seqshard_decode end to end (score pass, all_gather of (m_r, L_r), sampler + gather, "
                     f"all_reduce of the partials) over {args.dist_backend}; GB/s counts the K bytes of the "
                     "whole 512k sequence")}
+    if not args.share_gpu:
+        # the same step with both exchanges as one-shot peer-memory kernels (CUDA-IPC mapped buffers,
+        # NVLink P2P stores + flags); never with ranks sharing one GPU (they would wait on each other)
+        ex = sharding.PeerExchange(1 * H * d * 4, device=dev)
+
+        def full_peer(i):
+            sharding.seqshard_decode(q, loc.K, loc.V, seqlens, S, args.mode, args.seed, i, backend=be, ranges=ranges,
+                                     exchange=ex)
+        for i in range(3):
+            full_peer(i)
+        tp = max_over_ranks(timed_loop(full_peer, steps))
+        out["peer_exchange"] = {"us": round(tp * 1e3, 2), "GBps": round(kb / (tp * 1e-3) / 1e9, 1),
+                                "collectives_us": round(max(0.0, tp - t1 - t2) * 1e3, 2),
+                                "note": "santa_peer_allgather + santa_peer_allreduce_f32 instead of NCCL"}
+        ex.close()
     del loc, be
     torch.cuda.empty_cache()
     return out
+
+
+def peer_exchange_emulated(args, dev, timed_loop):
+    """The two config-4 exchange kernels on ONE GPU with every rank emulated in one cooperative launch
+    (local buffers, no NVLink): the kernels' own cost beside the NCCL-free path's latency budget."""
+    import torch
+
+    from paper_2605_01910_b200 import sharding
+    rows = {}
+    for R in (2, 4, 8):
+        grp = sharding.EmulatedPeerGroup(R, 32 * 128 * 4, device=dev)
+        st = [torch.randn(1, 32, 2, dtype=torch.float64, device=dev) for _ in range(R)]
+        pt = [torch.randn(1, 32, 128, device=dev) for _ in range(R)]
+        ta = timed_loop(lambda i: grp.all_gather(st), 50)
+        tr = timed_loop(lambda i: grp.all_reduce_(pt), 50)
+        rows[str(R)] = {"allgather_512B_us": round(ta * 1e3, 2), "allreduce_16KiB_us": round(tr * 1e3, 2)}
+    rows["note"] = ("all R ranks of the group in ONE launch on one GPU (EmulatedPeerGroup): kernel cost without "
+                    "NVLink; the multi-GPU run (n_local = 1 per rank) adds the P2P store latency")
+    return rows
 
 
 def main():
@@ -903,6 +937,7 @@ def main():
             res["config3"] = config3(args, dev, stream, timed_loop, max_over_ranks, peak, world)
         if world == 1:
             res["config4_per_rank"] = config4(args, dev, stream, timed_loop, peak)
+            res["config4_per_rank"]["peer_exchange_emulated"] = peer_exchange_emulated(args, dev, timed_loop)
             res["config5"] = config5(args, dev, stream, timed_loop, peak)
         else:
             res["config3_strong"] = config3_strong(args, dev, stream, timed_loop, max_over_ranks, peak, world, rank)

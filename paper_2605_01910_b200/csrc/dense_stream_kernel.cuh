@@ -344,23 +344,27 @@ __device__ __forceinline__ int dense_cta_of_stage(int s, int Stot, int grid) {
   return c;
 }
 
-// LSE merge of the split partials of one (b, h) in ONE pass over the slots: thread (d, part) runs an
-// online merge over its slots (running max, rescaled numerator and denominator; 16 slots' loads in
-// flight), then the parts are merged in fixed order.  (A max pass + weight pass + value pass cost
-// three dependent round trips: 9.4 us under ncu for 120 slots per head.)
+// LSE merge of the split partials of one (b, h) in ONE pass over the slots: CTA (h, d-slice)
+// of 512 threads = kDQ output coordinates x 16 parts; thread (d, part) runs an online merge over
+// its ~nslot/16 slots (all their loads in flight at once: one L2 round trip at config 2's ~114
+// slots per head), then the 16 parts are merged in fixed order.  (Round 2: 4 parts per coordinate
+// needed two dependent batches of 16 loads; a max pass + weight pass + value pass cost three round
+// trips -- 9.4 us under ncu for 120 slots per head.)
+constexpr int kDenseCombineThreads = 512, kDenseCombineParts = 16, kDQ = kDenseCombineThreads / kDenseCombineParts;
 template <typename T, int D, int G, int NW>
-__global__ void __launch_bounds__(512) dense_split_combine(DenseSplitParams p, int grid) {
-  constexpr int NTH = 512, NPART = NTH / D;
+__global__ void __launch_bounds__(kDenseCombineThreads) dense_split_combine(DenseSplitParams p, int grid) {
+  constexpr int NTH = kDenseCombineThreads, NPART = kDenseCombineParts;
   __shared__ float sM[NTH], sNum[NTH], sDen[NTH];
   pdl_wait_primary();
-  const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  constexpr int NSL = D / kDQ;
+  const int h = blockIdx.x / NSL, dsl = blockIdx.x - h * NSL, b = blockIdx.y, tid = threadIdx.x;
   const int kvh = h / G, gh = h - kvh * G;
   const int u = b * p.Hkv + kvh;
-  T* out = reinterpret_cast<T*>(p.out) + ((size_t)b * p.H + h) * D;
+  T* out = reinterpret_cast<T*>(p.out) + ((size_t)b * p.H + h) * D + dsl * kDQ;
   const int seqlen = __ldg(p.seqlens + b);
   if (seqlen < 1) {
-    for (int d = tid; d < D; d += NTH) out[d] = Elem<T>::from_f(0.f);
-    if (tid == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
+    for (int d = tid; d < kDQ; d += NTH) out[d] = Elem<T>::from_f(0.f);
+    if (tid == 0 && dsl == 0) atomicOr(p.flags, SANTA_FLAG_EMPTY_SEQ);
     return;
   }
   int Stot = 0, Pu = 0;
@@ -374,9 +378,9 @@ __global__ void __launch_bounds__(512) dense_split_combine(DenseSplitParams p, i
   const int c0 = dense_cta_of_stage(Pu, Stot, grid), c1 = dense_cta_of_stage(Pu + nu - 1, Stot, grid);
   const int nslot = (c1 - c0 + 1) * NW;
   const size_t slot0 = ((size_t)c0 + u) * NW;
-  const int d = tid % D, part = tid / D;
+  const int dl = tid % kDQ, part = tid / kDQ, d = dsl * kDQ + dl;
   float m = -INFINITY, num = 0.f, den = 0.f;
-  constexpr int U = 16;
+  constexpr int U = 8;
   for (int i0 = part; i0 < nslot; i0 += NPART * U) {
     float2 ml[U];
     float v[U];
@@ -406,15 +410,15 @@ __global__ void __launch_bounds__(512) dense_split_combine(DenseSplitParams p, i
   sNum[tid] = num;
   sDen[tid] = den;
   __syncthreads();
-  if (tid < D) {
+  if (tid < kDQ) {
     float ms = -INFINITY;
-    for (int q = 0; q < NPART; ++q) ms = fmaxf(ms, sM[q * D + tid]);
+    for (int q = 0; q < NPART; ++q) ms = fmaxf(ms, sM[q * kDQ + tid]);
     float sn = 0.f, sd = 0.f;
     for (int q = 0; q < NPART; ++q) {
-      const float mq = sM[q * D + tid];
+      const float mq = sM[q * kDQ + tid];
       const float r = mq > -INFINITY ? ex2(mq - ms) : 0.f;
-      sn = fmaf(r, sNum[q * D + tid], sn);
-      sd = fmaf(r, sDen[q * D + tid], sd);
+      sn = fmaf(r, sNum[q * kDQ + tid], sn);
+      sd = fmaf(r, sDen[q * kDQ + tid], sd);
     }
     out[tid] = Elem<T>::from_f(sn / sd);
   }

@@ -399,7 +399,11 @@ inline SampleParams make_sample_params(const DecodeArgs& a) {
   p.world = a.world;
   p.token_offset = a.token_offset;
   p.split_partial = nullptr;
-  p.trace = nullptr;
+  // tools only (tools/sample_trace.py): SANTA_SAMPLE_TRACE=<device address> of a [B*H][16] u64 buffer
+  // receives the sampler's per-phase globaltimer stamps; unset in every library use
+  static const unsigned long long trace_addr =
+      std::getenv("SANTA_SAMPLE_TRACE") ? std::strtoull(std::getenv("SANTA_SAMPLE_TRACE"), nullptr, 0) : 0ull;
+  p.trace = reinterpret_cast<unsigned long long*>(trace_addr);
   p.cluster = 1;
   return p;
 }

@@ -92,7 +92,13 @@ santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   while (CS < 4 && heads * CS * 2 <= 2 * num_sms() && CS * 2 <= a.S) CS *= 2;
   p.cluster = CS;
   const size_t smem = sample_smem_bytes(p.Cmax, (a.S + CS - 1) / CS, D, kSampleThreads);
-  if (ensure_smem(sample_gather_kernel<T, D, G>, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+  // more than two CTAs per SM needed for one wave: the 4-per-SM build (64 registers, 4 samples in
+  // flight per half-warp) -- config 5 (512 heads): see DESIGN.md sec. 5
+  static const int variant = std::getenv("SANTA_SAMPLE_MINB") ? std::atoi(std::getenv("SANTA_SAMPLE_MINB")) : 0;
+  const long ctas = (long)heads * CS;
+  const bool occ4 = variant == 4 || (variant == 0 && ctas > 2L * num_sms() && smem * 4 <= 200 * 1024);
+  auto kern = occ4 ? sample_gather_kernel<T, D, G, 4> : sample_gather_kernel<T, D, G, 1>;
+  if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
   if (a.events) cudaEventRecord(a.events[1], a.st);
   const bool pdl = a.events == nullptr && a.stats_all == nullptr;
   cudaLaunchConfig_t cfg = {};
@@ -114,7 +120,7 @@ santa_status RunSample<T, D, G>::run(const DecodeArgs& a) {
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  if (cudaLaunchKernelEx(&cfg, sample_gather_kernel<T, D, G>, p) != cudaSuccess) return SANTA_ERR_CUDA;
+  if (cudaLaunchKernelEx(&cfg, kern, p) != cudaSuccess) return SANTA_ERR_CUDA;
   if (a.events) cudaEventRecord(a.events[2], a.st);
   return SANTA_OK;
 }
@@ -302,8 +308,8 @@ santa_status RunDense<T, D, G>::run(const DecodeArgs& a) {
       const int grid = std::min(num_sms(), kDenseSplitMaxCtas);
       if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv, dp) != cudaSuccess)
         return SANTA_ERR_CUDA;
-      if (launch(dense_split_combine<T, D, G, NW>, dim3(a.g->n_heads, a.g->batch), dim3(512), 0, a.st, true, dp,
-                 grid) != cudaSuccess)
+      if (launch(dense_split_combine<T, D, G, NW>, dim3(a.g->n_heads * (D / kDQ), a.g->batch),
+                 dim3(kDenseCombineThreads), 0, a.st, true, dp, grid) != cudaSuccess)
         return SANTA_ERR_CUDA;
       return SANTA_OK;
     }

@@ -266,16 +266,157 @@ __device__ __forceinline__ void gather_chunk_rows_u(const SampleParams& p, int b
   __syncthreads();
 }
 
+// Two-phase form of gather_chunk_rows_u for register-capped builds (4 CTAs per SM): phase 1 finds
+// the in-chunk index of U samples per half-warp per round (their prefix blocks in flight together)
+// and parks J in sChunk; phase 2 loads U V rows per round.  With 16 samples per half-warp this is
+// 2 + 2 dependent memory round trips instead of 4 x (prefix block -> V row) = 8 for the fused loop
+// at U = 4 -- and only one U-deep buffer is live at a time.  Same ballots, same fixed-order sums.
+template <typename T, int D, bool kW, int U>
+__device__ __forceinline__ void gather_chunk_rows_2ph(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
+                                                      int Sl, int m_lo, int seqlen, int* sChunk, const float* sTl,
+                                                      float* sRed, float* sPart, const float* sWt, int idx_stride) {
+  const int NT = blockDim.x, NHW = NT >> 4;
+  const int tid = threadIdx.x;
+  const int S = idx_stride < 0 ? p.S : idx_stride;
+  constexpr int EB = (int)sizeof(T);
+  constexpr int VCH = D * EB / 16;
+  constexpr int NCH = (VCH + 15) / 16;
+  constexpr int EPC = 16 / EB;
+  const int hw = tid >> 4, l = tid & 15;
+  const unsigned hmask = 0xffffu << (threadIdx.x & 16);
+  const float* Pbase = p.stash + bh * p.stash_stride;
+  const int tok0 = p.token_offset ? __ldg(p.token_offset + b) : 0;
+  // ---- phase 1: J of every sample (L = 64 ballots; binary search for longer chunks) ----
+  for (int mw = 2 * (tid >> 5); mw < Sl; mw += NHW * U) {
+    const int m0 = mw + (hw & 1);
+    int cc[U], nn[U];
+    float4 pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NHW;
+      cc[u] = m < Sl ? sChunk[m] : -1;
+      nn[u] = cc[u] >= 0 ? min(p.L, seqlen - cc[u] * p.L) : 0;
+      pv[u] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+      if (cc[u] >= 0 && p.L == 64 && 4 * l < nn[u])
+        pv[u] = ldcg_f4(reinterpret_cast<const float4*>(Pbase + (size_t)cc[u] * p.L) + l);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NHW;
+      const bool on = cc[u] >= 0;
+      const float tf = on ? sTl[m] : -INFINITY;
+      const float4 v = pv[u];
+      int k;
+      if (p.L == 64) {
+        const int full_lanes = __popc(__ballot_sync(0xffffffffu, v.w <= tf) & hmask);
+        const int own = (v.x <= tf) + (v.y <= tf) + (v.z <= tf) + (v.w <= tf);
+        const int cross = __shfl_sync(0xffffffffu, own, (tid & 16) + min(full_lanes, 15));
+        k = full_lanes < 16 ? 4 * full_lanes + cross : 64;
+        if (__any_sync(0xffffffffu, on && k >= nn[u])) {
+          const int ln = max(nn[u] - 1, 0);
+          const int src = (tid & 16) + (ln >> 2);
+          const float tx = __shfl_sync(0xffffffffu, v.x, src), ty = __shfl_sync(0xffffffffu, v.y, src);
+          const float tz = __shfl_sync(0xffffffffu, v.z, src), tw = __shfl_sync(0xffffffffu, v.w, src);
+          const float tot = (ln & 3) == 0 ? tx : (ln & 3) == 1 ? ty : (ln & 3) == 2 ? tz : tw;
+          const int fl2 = __popc(__ballot_sync(0xffffffffu, v.w < tot) & hmask);
+          const int own2 = (v.x < tot) + (v.y < tot) + (v.z < tot) + (v.w < tot);
+          const int cross2 = __shfl_sync(0xffffffffu, own2, (tid & 16) + min(fl2, 15));
+          if (on && k >= nn[u]) k = fl2 < 16 ? 4 * fl2 + cross2 : nn[u] - 1;
+        }
+      } else {
+        k = 0;
+        if (on) {
+          const float* P = Pbase + (size_t)cc[u] * p.L;
+          k = thread_chunk_search(P, nn[u], tf);
+          if (k >= nn[u]) k = thread_chunk_search(P, nn[u], nextafterf(__ldcg(P + nn[u] - 1), -INFINITY));
+        }
+      }
+      const int j = on ? cc[u] * p.L + min(k, nn[u] - 1) : -1;
+      if (l == 0 && m < Sl) {
+        sChunk[m] = j;   // this half-warp's own sample: no other thread reads it before the barrier
+        if (p.idx_out) p.idx_out[bh * S + m_lo + m] = on ? j + tok0 : -1;
+      }
+    }
+  }
+  __syncthreads();
+  SANTA_TRACE(8);  // every J known (prefix blocks loaded, ballots done)
+  // ---- phase 2: V rows, U per half-warp in flight ----
+  float acc[NCH][EPC];
+#pragma unroll
+  for (int q = 0; q < NCH; ++q)
+#pragma unroll
+    for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
+  const T* Vb = reinterpret_cast<const T*>(p.V);
+  const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
+  for (int m0 = hw; m0 < Sl; m0 += NHW * U) {
+    uint4 raw[U][NCH];
+    float wt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int m = m0 + u * NHW;
+      const int j = m < Sl ? sChunk[m] : -1;
+      wt[u] = 1.f;
+      if constexpr (kW) wt[u] = j >= 0 ? sWt[m] : 0.f;
+      const T* row = j >= 0 ? (p.kv.page_table ? Vb + p.kv.row(b, kvh, j, D) : vbase + (int64_t)j * D) : nullptr;
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        const int ch = l + 16 * q;
+        raw[u][q] = (j >= 0 && ch < VCH) ? ldg_nc(row + ch * EPC) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < NCH; ++q) {
+        if constexpr (EB == 2) {
+          const uint32_t w[4] = {raw[u][q].x, raw[u][q].y, raw[u][q].z, raw[u][q].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if constexpr (kW) {
+              acc[q][2 * e] = fmaf(wt[u], Elem<T>::lo(w[e]), acc[q][2 * e]);
+              acc[q][2 * e + 1] = fmaf(wt[u], Elem<T>::hi(w[e]), acc[q][2 * e + 1]);
+            } else {
+              acc[q][2 * e] += Elem<T>::lo(w[e]);
+              acc[q][2 * e + 1] += Elem<T>::hi(w[e]);
+            }
+          }
+        } else {
+          acc[q][0] = fmaf(wt[u], __uint_as_float(raw[u][q].x), acc[q][0]);
+          acc[q][1] = fmaf(wt[u], __uint_as_float(raw[u][q].y), acc[q][1]);
+          acc[q][2] = fmaf(wt[u], __uint_as_float(raw[u][q].z), acc[q][2]);
+          acc[q][3] = fmaf(wt[u], __uint_as_float(raw[u][q].w), acc[q][3]);
+        }
+      }
+  }
+  SANTA_TRACE(9);  // V rows gathered and added (thread 0)
+#pragma unroll
+  for (int q = 0; q < NCH; ++q) {
+    const int ch = l + 16 * q;
+    if (ch < VCH)
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) sRed[hw * D + ch * EPC + e] = acc[q][e];
+  }
+  __syncthreads();
+  SANTA_TRACE(6);
+  for (int d = tid; d < D; d += NT) {
+    float s = 0.f;
+    for (int r = 0; r < NHW; ++r) s += sRed[r * D + d];
+    sPart[d] = s;
+  }
+  __syncthreads();
+}
+
 // U = samples in flight per half-warp.  U = 4 when one pass covers the work item (config 2: 4 per
 // half-warp): the unrolled U = 8 body is twice the code, half of it predicated off, and its
 // instruction fetch was the kernel's top stall (ncu `no_instructions` 52 %; sample phase 9.1 -> 8.1
 // us); U = 8 otherwise (flash at S = 2048: 36.9 vs 40.6 us with U = 4).
-template <typename T, int D, bool kW = false>
+template <typename T, int D, bool kW = false, int UMAX = 8>
 __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
                                                   int Sl, int m_lo, int seqlen, const int* sChunk,
                                                   const float* sTl, float* sRed, float* sPart,
                                                   const float* sWt = nullptr, int idx_stride = -1) {
-  if (Sl <= 4 * (int)(blockDim.x >> 4))
+  if (UMAX <= 4 || Sl <= 4 * (int)(blockDim.x >> 4))
     gather_chunk_rows_u<T, D, kW, 4>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, sWt,
                                      idx_stride);
   else
@@ -287,7 +428,7 @@ __device__ __forceinline__ void gather_chunk_rows(const SampleParams& p, int b, 
 // scaled by 1/S) in the returned shared array [D]; the caller reduces/scales/writes it.  All
 // threads of the block must call it.  Empty sequences (seqlen < 1) give a zero partial, idx -1
 // and the workspace flag.
-template <typename T, int D, int G>
+template <typename T, int D, int G, int UMAX = 8>
 __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int CS, unsigned char* smem_raw) {
   const int NT = blockDim.x, NW = NT >> 5, NHW = NT >> 4;
   const int kvh = h / G;
@@ -460,7 +601,11 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   SANTA_TRACE(5);
 
   // ---- a5 (part 2) + a6 ---------------------------------------------------------------------------
-  gather_chunk_rows<T, D>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart);
+  if constexpr (UMAX <= 4)
+    gather_chunk_rows_2ph<T, D, false, 8>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, nullptr,
+                                          -1);
+  else
+    gather_chunk_rows<T, D>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart);
   return sPart;
 }
 
@@ -492,15 +637,18 @@ __device__ __forceinline__ void finish_head(const SampleParams& p, size_t bh, in
   }
 }
 
-template <typename T, int D, int G>
-__global__ void __launch_bounds__(kSampleThreads, 1) sample_gather_kernel(SampleParams p) {
+// MINB = resident CTAs per SM the registers are capped for: 1 (default, 8 samples in flight per
+// half-warp) or 4 (<= 64 registers, 4 in flight): large batches (config 5: 512 heads = 512 CTAs)
+// fit in ONE wave at 4 CTAs per SM instead of two at 2.
+template <typename T, int D, int G, int MINB = 1>
+__global__ void __launch_bounds__(kSampleThreads, MINB) sample_gather_kernel(SampleParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   namespace cg = cooperative_groups;
   const int CS = p.cluster;
   const int rank = CS > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const int h = blockIdx.x / CS, b = blockIdx.y;
   const size_t bh = (size_t)b * p.H + h;
-  float* sPart = sample_item<T, D, G>(p, b, h, rank, CS, smem_raw);
+  float* sPart = sample_item<T, D, G, (MINB >= 3 ? 4 : 8)>(p, b, h, rank, CS, smem_raw);
   finish_head<T, D>(p, bh, rank, CS, sPart);
   if (p.trace && threadIdx.x == 0 && rank == 0) p.trace[bh * 16 + 7] = gtimer();
 }

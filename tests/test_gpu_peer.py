@@ -20,7 +20,7 @@ import torch.multiprocessing as mp
 import paper_2605_01910_b200 as santa
 from paper_2605_01910_b200 import sharding
 import santa_inputs as si
-from gpu_helpers import unit_parity
+from test_gpu_fullsize import unit_parity
 
 pytestmark = pytest.mark.gpu
 
