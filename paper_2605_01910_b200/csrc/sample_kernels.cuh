@@ -271,7 +271,7 @@ __device__ __forceinline__ void gather_chunk_rows_u(const SampleParams& p, int b
 // and parks J in sChunk; phase 2 loads U V rows per round.  With 16 samples per half-warp this is
 // 2 + 2 dependent memory round trips instead of 4 x (prefix block -> V row) = 8 for the fused loop
 // at U = 4 -- and only one U-deep buffer is live at a time.  Same ballots, same fixed-order sums.
-template <typename T, int D, bool kW, int U>
+template <typename T, int D, bool kW, int U, int U2 = U>
 __device__ __forceinline__ void gather_chunk_rows_2ph(const SampleParams& p, int b, int h, int rank, int kvh, size_t bh,
                                                       int Sl, int m_lo, int seqlen, int* sChunk, const float* sTl,
                                                       float* sRed, float* sPart, const float* sWt, int idx_stride) {
@@ -349,11 +349,11 @@ __device__ __forceinline__ void gather_chunk_rows_2ph(const SampleParams& p, int
     for (int e = 0; e < EPC; ++e) acc[q][e] = 0.f;
   const T* Vb = reinterpret_cast<const T*>(p.V);
   const T* vbase = p.kv.page_table ? Vb : Vb + ((int64_t)b * p.kv.n_kv_heads + kvh) * p.kv.page_size * D;
-  for (int m0 = hw; m0 < Sl; m0 += NHW * U) {
-    uint4 raw[U][NCH];
-    float wt[U];
+  for (int m0 = hw; m0 < Sl; m0 += NHW * U2) {
+    uint4 raw[U2][NCH];
+    float wt[U2];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+    for (int u = 0; u < U2; ++u) {
       const int m = m0 + u * NHW;
       const int j = m < Sl ? sChunk[m] : -1;
       wt[u] = 1.f;
@@ -366,7 +366,7 @@ __device__ __forceinline__ void gather_chunk_rows_2ph(const SampleParams& p, int
       }
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
+    for (int u = 0; u < U2; ++u)
 #pragma unroll
       for (int q = 0; q < NCH; ++q) {
         if constexpr (EB == 2) {
@@ -601,8 +601,8 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   SANTA_TRACE(5);
 
   // ---- a5 (part 2) + a6 ---------------------------------------------------------------------------
-  if constexpr (UMAX <= 4)
-    gather_chunk_rows_2ph<T, D, false, 8>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, nullptr,
+  if constexpr (UMAX <= 4)  // 4 prefix blocks, then 8 V rows in flight per half-warp: no spills at 64 registers
+    gather_chunk_rows_2ph<T, D, false, 4, 8>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart, nullptr,
                                           -1);
   else
     gather_chunk_rows<T, D>(p, b, h, rank, kvh, bh, Sl, m_lo, seqlen, sChunk, sTl, sRed, sPart);
@@ -638,8 +638,10 @@ __device__ __forceinline__ void finish_head(const SampleParams& p, size_t bh, in
 }
 
 // MINB = resident CTAs per SM the registers are capped for: 1 (default, 8 samples in flight per
-// half-warp) or 4 (<= 64 registers, 4 in flight): large batches (config 5: 512 heads = 512 CTAs)
-// fit in ONE wave at 4 CTAs per SM instead of two at 2.
+// half-warp, fused prefix-block -> V-row loop) or 4 (<= 64 registers, two-phase gather: 4 prefix
+// blocks, then 8 V rows in flight per half-warp -- no spills; (8, 8) spilled 160 B and ran 5 us slower
+// at config 5): large batches (config 5: 512 heads = 512 CTAs) fit in ONE wave at 4 CTAs per SM
+// instead of two at 2 (config 5 175.6 -> 162.1 us).
 template <typename T, int D, int G, int MINB = 1>
 __global__ void __launch_bounds__(kSampleThreads, MINB) sample_gather_kernel(SampleParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];

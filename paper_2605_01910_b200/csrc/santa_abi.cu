@@ -155,11 +155,11 @@ int auto_path(const santa_geometry* g, int S) {
   const bool step_ok = g->dtype != SANTA_F32 && g->max_seqlen <= 65536;
   const bool tc_pages = !g->page_table || g->page_size % kTcTileKeys == 0;
   if (step_ok && (int64_t)g->batch * g->n_heads >= kTcMinHeads) {
-    // batch 32 (tools/path_sweep.py, profiles/r01_v10_path_sweep_*.json): S <= 256 the tcgen05 step
-    // kernel (367 / 383-393 us at S = 64 / 256), S = 512 the mma.sync step kernel (419 vs 437 us for
-    // the two-kernel path, 458 for tcgen05)
-    if (S <= 256 && tc_pages) return SANTA_PATH_STEP_TC;
-    if (S > 256 && S <= 512) return SANTA_PATH_STEP_KERNEL;
+    // batch 32 (tools/path_sweep.py, profiles/r02/v49_path_sweep.json): since the 4-CTA-per-SM
+    // sampler the two-kernel path wins from S = 256 (389 vs 396 us for tcgen05 at S = 256, 413 vs 422
+    // us for the mma.sync step kernel at S = 512); at S = 64 the tcgen05 step kernel still samples
+    // under the stream for less (365 vs 369 us)
+    if (S <= 64 && tc_pages) return SANTA_PATH_STEP_TC;
   }
   return SANTA_PATH_TWO_KERNEL;
 }

@@ -103,12 +103,12 @@ def test_product_package_never_imports_the_oracle():
 
 
 def test_auto_path_policy_is_host_logic():
-    """santa_auto_path (pure host arithmetic): the two-kernel path below 1024 query heads or for
-    S > 512 / fp32 / long contexts; from 1024 heads the tcgen05 step kernel for S <= 256 and the
-    mma.sync step kernel for 256 < S <= 512."""
+    """santa_auto_path (pure host arithmetic): the two-kernel path except from 1024 query heads with
+    S <= 64 (the tcgen05 step kernel), measured in profiles/r02/v49_path_sweep.json."""
     assert santa.santa_auto_path(_geo(), 256) == "two_kernel"             # config 2
-    assert santa.santa_auto_path(_geo(batch=32), 256) == "step_tc"        # config 3
-    assert santa.santa_auto_path(_geo(batch=32), 512) == "step"
+    assert santa.santa_auto_path(_geo(batch=32), 64) == "step_tc"         # config 3, S = 64
+    assert santa.santa_auto_path(_geo(batch=32), 256) == "two_kernel"     # config 3, S = 256
+    assert santa.santa_auto_path(_geo(batch=32), 512) == "two_kernel"
     assert santa.santa_auto_path(_geo(batch=32), 1024) == "two_kernel"
     assert santa.santa_auto_path(_geo(batch=32, dtype=1), 256) == "two_kernel"   # fp32 cache
     assert santa.santa_auto_path(_geo(batch=32, max_seqlen=131072), 256) == "two_kernel"
