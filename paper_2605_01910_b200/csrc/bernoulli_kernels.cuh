@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
   };
 
   float* w = p.w + unit * G * D;
+  __shared__ float sWt[G * D];  // the weights and the selection again in shared memory: the fragment
+  __shared__ int sSel[D];       // loop below reads them (from global it was a chain of L2 round trips)
   bool selected = false;
   if (p.mean_group) {
     double m = 0.0;
@@ -109,7 +111,11 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
     selected = c > 0 && m > 0.0;
     const double mhat = norm * (double)c / (double)p.nB;
 #pragma unroll
-    for (int g = 0; g < G; ++g) w[g * D + i] = selected ? (float)((mhat * qd[g]) / m) : 0.f;
+    for (int g = 0; g < G; ++g) {
+      const float wv = selected ? (float)((mhat * qd[g]) / m) : 0.f;
+      w[g * D + i] = wv;
+      sWt[g * D + i] = wv;
+    }
     if (p.feature_mask) p.feature_mask[unit * D + i] = selected ? 1 : 0;
   } else {
 #pragma unroll
@@ -118,7 +124,9 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
       int c = 0;
       if (norm > 0.0) c = counts(fabs(qd[g]) / norm, kTagBernoulliHead, (uint32_t)(p.head_offset + kvh * G + g));
       const double sg = qd[g] > 0.0 ? 1.0 : (qd[g] < 0.0 ? -1.0 : 0.0);
-      w[g * D + i] = c ? (float)((norm / (double)p.nB) * (double)c * sg) : 0.f;
+      const float wv = c ? (float)((norm / (double)p.nB) * (double)c * sg) : 0.f;
+      w[g * D + i] = wv;
+      sWt[g * D + i] = wv;
       selected |= c > 0;
       if (p.feature_mask) p.feature_mask[((size_t)b * p.H + kvh * G + g) * D + i] = c > 0 ? 1 : 0;
     }
@@ -131,7 +139,11 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
   __syncthreads();
   int base = 0;
   for (int k = 0; k < (i >> 5); ++k) base += sWarpCnt[k];
-  if (selected) p.sel[unit * D + base + __popc(bal & ((1u << (i & 31)) - 1u))] = i;
+  if (selected) {
+    const int pos = base + __popc(bal & ((1u << (i & 31)) - 1u));
+    p.sel[unit * D + pos] = i;
+    sSel[pos] = i;
+  }
   if (i == D - 1) {
     int tot = 0;
     for (int k = 0; k < D / 32; ++k) tot += sWarpCnt[k];
@@ -140,18 +152,17 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
   if (p.wfrag != nullptr) {
     // m16n8k16 B fragments of the weights in selection order (bern_tma_kernel): group kg of 16
     // selected features, part q of the 3-way bf16 split, lane (g, t) = (head g, features 2t, 2t+1
-    // and 2t+8, 2t+9); heads >= G and features past |F| are 0.  The sel / w stores above are
-    // visible to the block after the barrier.
+    // and 2t+8, 2t+9); heads >= G and features past |F| are 0.  sWt / sSel (shared) are
+    // complete after the barrier.
     __syncthreads();
     int nsel = 0;
     for (int k = 0; k < D / 32; ++k) nsel += sWarpCnt[k];
-    const int* sel = p.sel + unit * D;
     uint2* wf = p.wfrag + unit * (D / 16) * 96;
     for (int e = i; e < (D / 16) * 96; e += D) {
       const int kg = e / 96, q = (e / 32) % 3, ln = e % 32;
       const int g = ln >> 2, s0 = 16 * kg + 2 * (ln & 3);
       auto part = [&](int s) -> uint32_t {
-        return (g < G && s < nsel) ? (uint32_t)bern_weight_part(w[g * D + sel[s]], q) : 0u;
+        return (g < G && s < nsel) ? (uint32_t)bern_weight_part(sWt[g * D + sSel[s]], q) : 0u;
       };
       wf[e] = make_uint2(part(s0) | (part(s0 + 1) << 16), part(s0 + 8) | (part(s0 + 9) << 16));
     }
