@@ -22,10 +22,26 @@
 
 namespace santa {
 
-constexpr int kDenseStageKeys = 32;     // keys per stage (K + V = 16 KiB at d = 128)
-constexpr int kDenseWarps = 6;
-constexpr int kDenseSlots = 2;
-constexpr int kPRow = 40;  // padded bf16 row of the per-warp P buffer (conflict-free B-fragment loads)
+// 32-key stages, 3 consumer warps x 4 ring slots (192 KiB in flight per SM) below ~4 MiB of K+V per SM:
+// config 2 28.0 us vs 29.6-29.9 for 6 x 2, 28.2-28.3 for 5 x 2 / 4 x 3 / 64-key 3 x 2, 29.2 for 64-key 6 x 1, 30.4 for 2 x 6 (A/B builds,
+// profiles/r02/v54-v56_dense_ab.txt) -- fewer warps: fewer split partials to merge and less ring contention
+#ifndef SANTA_DENSE_SK  // (tools: A/B builds override the three)
+#define SANTA_DENSE_SK 32
+#define SANTA_DENSE_NW 3
+#define SANTA_DENSE_SPW 4
+#endif
+constexpr int kDenseStageKeys = SANTA_DENSE_SK;  // keys per stage (K + V = 16 KiB at d = 128, 32 keys)
+constexpr int kDenseWarps = SANTA_DENSE_NW;
+constexpr int kDenseSlots = SANTA_DENSE_SPW;
+// >= 4 MiB of K+V per SM (config 3, 4 GiB): 5 warps x 2 slots 631-633 us vs 672-674 for 6 x 2, 646-658 for
+// 4 x 3, 674-676 for 3 x 4 (profiles/r02/v62_dense_large_ab.txt; cuDNN SDPA 600 us)
+#ifndef SANTA_DENSE_NWL  // (tools: A/B builds override both)
+#define SANTA_DENSE_NWL 5
+#define SANTA_DENSE_SPWL 2
+#endif
+constexpr int kDenseWarpsLarge = SANTA_DENSE_NWL, kDenseSlotsLarge = SANTA_DENSE_SPWL;  // >= 4 MiB of K+V per SM
+constexpr int kDenseWarpsMax = kDenseWarps > kDenseWarpsLarge ? kDenseWarps : kDenseWarpsLarge;
+constexpr int kPRow = kDenseStageKeys + 8;  // padded bf16 row of the per-warp P buffer (conflict-free B loads)
 
 __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
@@ -350,10 +366,13 @@ __device__ __forceinline__ int dense_cta_of_stage(int s, int Stot, int grid) {
 // slots per head), then the 16 parts are merged in fixed order.  (Round 2: 4 parts per coordinate
 // needed two dependent batches of 16 loads; a max pass + weight pass + value pass cost three round
 // trips -- 9.4 us under ncu for 120 slots per head.)
-constexpr int kDenseCombineThreads = 512, kDenseCombineParts = 16, kDQ = kDenseCombineThreads / kDenseCombineParts;
-template <typename T, int D, int G, int NW>
+// NPART = 512 / D (one CTA per head) when a head has few slots (config 3: ~1-2 CTAs per unit), else 16.
+constexpr int kDenseCombineThreads = 512;
+template <typename T, int D, int G, int NW, int NPART>
 __global__ void __launch_bounds__(kDenseCombineThreads) dense_split_combine(DenseSplitParams p, int grid) {
-  constexpr int NTH = kDenseCombineThreads, NPART = kDenseCombineParts;
+  constexpr int NTH = kDenseCombineThreads;
+  constexpr int kDQ = NTH / NPART;  // output coordinates per CTA
+  static_assert(kDQ <= D && D % kDQ == 0, "combine slice");
   __shared__ float sM[NTH], sNum[NTH], sDen[NTH];
   pdl_wait_primary();
   constexpr int NSL = D / kDQ;

@@ -103,7 +103,7 @@ inline WsLayout layout(const santa_geometry* g, int S) {
   L.step_rec = off; off = align256(off + B * H * (size_t)L.Cmax * 16);
   L.step_stash = off; off = align256(off + B * H * (size_t)L.Cmax * 64 * 4);
   L.step_part = off; off = align256(off + B * H * (size_t)kStepMaxSplits * D * 8);
-  const size_t dslots = ((size_t)kDenseSplitMaxCtas + B * Hkv) * kDenseWarps;  // dense_split_kernel slots
+  const size_t dslots = ((size_t)kDenseSplitMaxCtas + B * Hkv) * kDenseWarpsMax;  // dense_split_kernel slots
   L.dense_o = off; off = align256(off + dslots * G * D * 4);
   L.dense_ml = off; off = align256(off + dslots * G * 8);
   L.total = off;

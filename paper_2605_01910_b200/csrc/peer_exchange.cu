@@ -172,13 +172,16 @@ santa_status run(const santa_peer_group* g, int32_t n_local, const int32_t* rank
   a.slot = slot;
   a.epoch = epoch;
   a.op = op;
-  // cooperative: with n_local > 1 (all ranks of a group emulated in one launch on one GPU) the
-  // CTAs wait on one another, so they must be co-resident -- which a cooperative launch guarantees
-  // (or refuses); with n_local == 1 they only wait on other GPUs.
+  // cooperative when n_local > 1 (all ranks of a group emulated in one launch on one GPU): the CTAs
+  // wait on one another, so they must be co-resident -- which a cooperative launch guarantees (or
+  // refuses); with n_local == 1 they only wait on other GPUs and a plain launch is cheaper.
   void* args[] = {&a};
-  const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(peer_exchange_kernel),
-                                                    dim3((unsigned)nblk, (unsigned)n_local), dim3(kThreads), args, 0,
-                                                    static_cast<cudaStream_t>(stream));
+  const dim3 grid((unsigned)nblk, (unsigned)n_local);
+  const cudaError_t e =
+      n_local > 1 ? cudaLaunchCooperativeKernel(reinterpret_cast<void*>(peer_exchange_kernel), grid, dim3(kThreads),
+                                                args, 0, static_cast<cudaStream_t>(stream))
+                  : cudaLaunchKernel(reinterpret_cast<void*>(peer_exchange_kernel), grid, dim3(kThreads), args, 0,
+                                     static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) {
     cudaGetLastError();
     return SANTA_ERR_CUDA;

@@ -20,7 +20,7 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
     const size_t smem = 1024 + (size_t)NW * G * p.L * 4 + (size_t)NW * SPW * (kStageBytes + 16);
     if (smem <= 220 * 1024) {  // else: per-warp score buffers too large (G * L big) -> fallback kernel
     const int total = a.g->batch * a.g->n_kv_heads * p.Cmax;
-    const int grid = total < num_sms() ? total : num_sms();
+    const int grid = total < num_sms() * SANTA_STREAM_CTAS ? total : num_sms() * SANTA_STREAM_CTAS;
     if (a.k_new) {  // the fused KV append (santa_decode_attention_append)
       auto kern = score_stream_append_kernel<T, D, G, NW, SPW>;
       if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
@@ -262,6 +262,49 @@ santa_status RunStep<T, D, G>::run(const DecodeArgs& a) {
   }
 }
 
+template <typename T, int D, int G, int NW, int SPW>
+santa_status run_dense_split(const DecodeArgs& a, const DenseParams& p) {
+  constexpr size_t kStageBytes = 2 * (D / 64) * kDenseStageKeys * 128;
+  const size_t smem = 1024 + (size_t)NW * SPW * (kStageBytes + 16) + (size_t)NW * 8 * kPRow * 2;
+  auto kern = dense_split_kernel<T, D, G, NW, SPW>;
+  if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
+  CUtensorMap tk, tv;
+  const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
+                                        : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
+  if (!make_kmap(&tk, a.K, rows, D, a.g->dtype, kDenseStageKeys) ||
+      !make_kmap(&tv, a.V, rows, D, a.g->dtype, kDenseStageKeys))
+    return SANTA_ERR_CUDA;
+  DenseSplitParams dp;
+  dp.q = a.q;
+  dp.kv = p.kv;
+  dp.seqlens = a.seqlens;
+  dp.B = p.B;
+  dp.H = p.H;
+  dp.Hkv = p.Hkv;
+  dp.scale_log2 = p.scale_log2;
+  dp.part_o = at<float>(a.ws, a.L.dense_o);
+  dp.part_ml = at<float2>(a.ws, a.L.dense_ml);
+  dp.out = a.out;
+  dp.flags = p.flags;
+  const int grid = std::min(num_sms(), kDenseSplitMaxCtas);
+  if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv, dp) != cudaSuccess)
+    return SANTA_ERR_CUDA;
+  // slots per head ~ (CTAs per unit + 1) x NW: 16 parts per output coordinate when that is large
+  // (config 2: ~19 CTAs per unit -> one L2 round trip), else one 4-part CTA per head (config 3)
+  const int units = a.g->batch * a.g->n_kv_heads;
+  const bool many = (grid / units + 1) * NW >= 32;
+  constexpr int NPB = 16, NPS = kDenseCombineThreads / D;  // NPS: one CTA per head
+  const cudaError_t e =
+      many ? launch(dense_split_combine<T, D, G, NW, NPB>, dim3(a.g->n_heads * (D * NPB / kDenseCombineThreads),
+                                                                  a.g->batch),
+                    dim3(kDenseCombineThreads), 0, a.st, true, dp, grid)
+           : launch(dense_split_combine<T, D, G, NW, NPS>, dim3(a.g->n_heads * (D * NPS / kDenseCombineThreads),
+                                                                  a.g->batch),
+                    dim3(kDenseCombineThreads), 0, a.st, true, dp, grid);
+  if (e != cudaSuccess) return SANTA_ERR_CUDA;
+  return SANTA_OK;
+}
+
 template <typename T, int D, int G>
 santa_status RunDense<T, D, G>::run(const DecodeArgs& a) {
   DenseParams p;
@@ -282,36 +325,11 @@ santa_status RunDense<T, D, G>::run(const DecodeArgs& a) {
   bool done = false;
   if constexpr (sizeof(T) == 2) {
     if (stream_eligible(a.g)) {  // balanced split-KV tensor-core kernel + its LSE combine
-      constexpr int NW = kDenseWarps, SPW = kDenseSlots;
-      constexpr size_t kStageBytes = 2 * (D / 64) * kDenseStageKeys * 128;
-      const size_t smem = 1024 + (size_t)NW * SPW * (kStageBytes + 16) + (size_t)NW * 8 * kPRow * 2;
-      auto kern = dense_split_kernel<T, D, G, NW, SPW>;
-      if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
-      CUtensorMap tk, tv;
-      const uint64_t rows = a.g->page_table ? (uint64_t)0x7fffffff
-                                            : (uint64_t)a.g->batch * a.g->n_kv_heads * a.g->max_seqlen;
-      if (!make_kmap(&tk, a.K, rows, D, a.g->dtype, kDenseStageKeys) ||
-          !make_kmap(&tv, a.V, rows, D, a.g->dtype, kDenseStageKeys))
-        return SANTA_ERR_CUDA;
-      DenseSplitParams dp;
-      dp.q = a.q;
-      dp.kv = p.kv;
-      dp.seqlens = a.seqlens;
-      dp.B = p.B;
-      dp.H = p.H;
-      dp.Hkv = p.Hkv;
-      dp.scale_log2 = p.scale_log2;
-      dp.part_o = at<float>(a.ws, a.L.dense_o);
-      dp.part_ml = at<float2>(a.ws, a.L.dense_ml);
-      dp.out = a.out;
-      dp.flags = p.flags;
-      const int grid = std::min(num_sms(), kDenseSplitMaxCtas);
-      if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv, dp) != cudaSuccess)
-        return SANTA_ERR_CUDA;
-      if (launch(dense_split_combine<T, D, G, NW>, dim3(a.g->n_heads * (D / kDQ), a.g->batch),
-                 dim3(kDenseCombineThreads), 0, a.st, true, dp, grid) != cudaSuccess)
-        return SANTA_ERR_CUDA;
-      return SANTA_OK;
+      // warps x slots by the bytes each SM streams: 3 x 4 below ~4 MiB per SM (config 2: 28.0 vs 29.7
+      // us for 6 x 2 -- fewer partials to merge), 5 x 2 above (config 3, 4 GiB: 631 vs 672 us for 6 x 2)
+      const double per_sm = 2.0 * a.g->batch * a.g->n_kv_heads * (double)a.g->max_seqlen * D * sizeof(T) / num_sms();
+      return per_sm < 4.0 * (1 << 20) ? run_dense_split<T, D, G, kDenseWarps, kDenseSlots>(a, p)
+                                      : run_dense_split<T, D, G, kDenseWarpsLarge, kDenseSlotsLarge>(a, p);
     }
   }
   if (!done) {

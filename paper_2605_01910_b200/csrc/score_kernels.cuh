@@ -247,8 +247,18 @@ __device__ __forceinline__ void store_tile_scores(float* sS, int L, int key0, in
 // producer issues a group's stages round-robin over the warps (round s: stage s of chunks
 // 0..NW-1), so all warps stream in parallel for any L.
 // dynamic smem: [NW*SPW][D/64][64 rows x 128 B] ring (1024-B aligned) | sS[NW][G][L] | barriers
-constexpr int kStreamWarps = 6;  // default consumer warps (tuned with tools/microbench_score.cu)
-constexpr int kStreamSlots = 2;  // default ring slots per consumer warp
+// 5 consumer warps x 2 slots (A/B builds, profiles/r02/v61_score_stream_ab.txt): config 2 pass 14.5-14.6 vs
+// 14.8 us for 6 x 2, config 3 (2 GiB) 339-340 vs 349-351 us; 4 x 3 / 3 x 4 16.4 / 16.5 us; two CTAs per SM
+// (3 x 2 / 2 x 3 each) 16.4 / 18.5 us at config 2
+#ifndef SANTA_STREAM_NW  // (tools: A/B builds override these)
+#define SANTA_STREAM_NW 5
+#define SANTA_STREAM_SPW 2
+#endif
+#ifndef SANTA_STREAM_CTAS
+#define SANTA_STREAM_CTAS 1  // persistent CTAs per SM
+#endif
+constexpr int kStreamWarps = SANTA_STREAM_NW;   // default consumer warps (tuned with tools/microbench_score.cu)
+constexpr int kStreamSlots = SANTA_STREAM_SPW;  // default ring slots per consumer warp
 
 // Incremental walk over a strided chunk sequence (no divisions in the loop):
 // w -> (c = w % Cmax, unit = w / Cmax), w += step.
