@@ -115,9 +115,15 @@ __device__ __forceinline__ double block_excl_scan_d(double v, double* sred, doub
   return off + incl - v;
 }
 
+// Skewed index of chunk c in sample_item's per-chunk fp64 tables: thread t owns the contiguous chunks
+// [t per, t per + per), so unskewed 8-B entries put a warp's 32 threads in one bank group (a 32-way
+// conflict per access -- 19.5 us of fp64 CDF build at 4096 chunks, config 4 phase 2 at R = 2); one pad
+// entry per 16 spreads them.
+__host__ __device__ __forceinline__ int cskew(int c) { return c + (c >> 4); }
+
 // Shared-memory bytes sample_item needs for a CTA of nthreads threads.
 __host__ __device__ inline size_t sample_smem_bytes(int Cmax, int S_local, int D, int nthreads) {
-  return (size_t)Cmax * 16 + (size_t)S_local * 16 + (size_t)(nthreads / 16 + 1) * D * 4 + 64;
+  return (size_t)cskew(Cmax) * 16 + 16 + (size_t)S_local * 16 + (size_t)(nthreads / 16 + 1) * D * 4 + 64;
 }
 
 // a5 (part 2) + a6 for the Sl samples of one work item whose chunk sChunk[m] (-1: not sampled
@@ -438,10 +444,11 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   const int m_lo = (int)((long long)S * rank / CS), m_hi = (int)((long long)S * (rank + 1) / CS);
   const int Sl = m_hi - m_lo;                           // strata owned by this item
   const int Slmax = (S + CS - 1) / CS;
-  double* sF = reinterpret_cast<double*>(smem_raw);     // [Cmax] chunk CDF
-  double* sT = sF + p.Cmax;                             // [Slmax] thresholds
-  float2* sC = reinterpret_cast<float2*>(sT + Slmax);   // [Cmax] chunk stats, then rescale (double)
-  int* sChunk = reinterpret_cast<int*>(sC + p.Cmax);    // [Slmax]
+  const int CmaxS = cskew(p.Cmax) + 1;                  // skewed table length (index cskew(c))
+  double* sF = reinterpret_cast<double*>(smem_raw);     // [CmaxS] chunk CDF
+  double* sT = sF + CmaxS;                              // [Slmax] thresholds
+  float2* sC = reinterpret_cast<float2*>(sT + Slmax);   // [CmaxS] chunk stats, then rescale (double)
+  int* sChunk = reinterpret_cast<int*>(sC + CmaxS);     // [Slmax]
   float* sTl = reinterpret_cast<float*>(sChunk + Slmax);  // [Slmax]
   float* sRed = sTl + Slmax;                            // [NHW][D]
   float* sPart = sRed + NHW * D;                        // [D]
@@ -498,9 +505,9 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
       if (c0 + i >= c1) break;
       const float w32 = st[i].y > 0.f ? ex2(st[i].x - mstar) : 0.f;  // 2^(m_c - m*)
       const double w = (double)w32 * (double)st[i].y;
-      sF[c0 + i] = w;
+      sF[cskew(c0 + i)] = w;
       // in-chunk rescale Z 2^(m* - m_c) = Z l_c / W_c: store 1 / 2^(m_c - m*) now, times Z below
-      reinterpret_cast<double*>(sC)[c0 + i] = w > 0.0 ? 1.0 / (double)w32 : 0.0;
+      reinterpret_cast<double*>(sC)[cskew(c0 + i)] = w > 0.0 ? 1.0 / (double)w32 : 0.0;
       part += w;
       if (w > 0.0) lastpos = c0 + i;
     }
@@ -508,23 +515,23 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
     float mloc = -INFINITY;
     for (int c = tid; c < nC; c += NT) {
       const float2 v = __ldcg(cs + c);
-      sC[c] = v;
+      sC[cskew(c)] = v;
       mloc = fmaxf(mloc, v.x);
     }
     const float mstar = block_max_f(mloc, sred_f);  // (its barrier also publishes sC)
     SANTA_TRACE(3);
     for (int c = c0; c < c1; ++c) {
-      const float2 st = sC[c];
+      const float2 st = sC[cskew(c)];
       const float w32 = st.y > 0.f ? ex2(st.x - mstar) : 0.f;
       const double w = (double)w32 * (double)st.y;
-      sF[c] = w;
+      sF[cskew(c)] = w;
       part += w;
       if (w > 0.0) lastpos = c;
     }
     __syncthreads();  // every thread has read its sC entries before they are overwritten
     for (int c = c0; c < c1; ++c) {
-      const double w = sF[c];
-      reinterpret_cast<double*>(sC)[c] = w > 0.0 ? (double)sC[c].y / w : 0.0;  // l_c / W_c
+      const double w = sF[cskew(c)];
+      reinterpret_cast<double*>(sC)[cskew(c)] = w > 0.0 ? (double)sC[cskew(c)].y / w : 0.0;  // l_c / W_c
     }
   }
   double Z;
@@ -532,10 +539,10 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   lastpos = block_max_i(lastpos, sred_i);
   const double invZ = 1.0 / Z;
   for (int c = c0; c < c1; ++c) {
-    const double w = sF[c];
+    const double w = sF[cskew(c)];
     run += w;
-    sF[c] = c >= lastpos ? 1.0 : run * invZ;
-    reinterpret_cast<double*>(sC)[c] *= Z;  // Z l_c / W_c
+    sF[cskew(c)] = c >= lastpos ? 1.0 : run * invZ;
+    reinterpret_cast<double*>(sC)[cskew(c)] *= Z;  // Z l_c / W_c
   }
   SANTA_TRACE(4);
   // ---- sequence sharding: this rank's slice of the global shard CDF --------------------------
@@ -588,11 +595,11 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
       int lo = 0, hi = nC - 1;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (sF[mid] > Tm) hi = mid; else lo = mid + 1;
+        if (sF[cskew(mid)] > Tm) hi = mid; else lo = mid + 1;
       }
       c = lo;
-      const double Fprev = c ? sF[c - 1] : 0.0;
-      tl = __double2float_rd((Tm - Fprev) * reinterpret_cast<const double*>(sC)[c]);
+      const double Fprev = c ? sF[cskew(c - 1)] : 0.0;
+      tl = __double2float_rd((Tm - Fprev) * reinterpret_cast<const double*>(sC)[cskew(c)]);
     }
     sChunk[m] = c;
     sTl[m] = tl;

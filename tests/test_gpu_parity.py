@@ -338,3 +338,21 @@ def test_odd_chunk_strides_and_unaligned_stats_rows():
     inp = to_cuda(si.make_decode_inputs(3, 16, 4, 128, [20000, 16447, 19000], dtype="bf16", seed=63))
     out, idx = gpu_decode(inp, 192, "stratified", seed=5)
     REPORT.append(("odd-Cmax", 0, "auto", check_parity(inp, out, idx, 192, "stratified", 5)))
+
+
+@pytest.mark.parametrize("B,n,units", [(1, 32768, [(0, 0), (0, 7)]), (4, [40000, 39001, 40000, 12345],
+                                                                       [(0, 3), (1, 7), (3, 0)])])
+def test_dense_reference_split_shapes(B, n, units):
+    """The split-KV dense kernel in both of its shapes: config 2 (3 warps x 4 slots, 16-part LSE
+    combine: ~19 CTAs per unit) and above 4 MiB of K+V per SM (5 warps x 2 slots, one combine CTA per
+    head), against the fp64 dense oracle on sampled (b, kv-head) units incl. a ragged last stage."""
+    inp = si.make_decode_inputs(B, 32, 8, 128, n, dtype="bf16", seed=14, workload="temp4", device="cuda")
+    out = santa.dense(inp.q, inp.K, inp.V, inp.seqlens)
+    torch.cuda.synchronize()
+    lens = inp.seqlens.cpu().numpy()
+    for b, kvh in units:
+        hs = slice(4 * kvh, 4 * kvh + 4)
+        ref = o.dense_decode(si.as_bits(inp.q[b:b + 1, hs]), si.as_bits(inp.K[b:b + 1, kvh:kvh + 1]),
+                             si.as_bits(inp.V[b:b + 1, kvh:kvh + 1]), lens[b:b + 1])
+        err = np.abs(out[b:b + 1, hs].float().cpu().numpy() - ref).max()
+        assert err <= 2e-2, (b, kvh, err)

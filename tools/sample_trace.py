@@ -13,7 +13,10 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 CFG = int(os.environ.get("CFG", "5"))
+R = int(os.environ.get("R", "2"))  # CFG=4: rank 0's phase 2 of a 512k sequence sharded over R ranks
 B, H, Hkv, d, n, S = (16 if CFG == 5 else 32), 32, 8, 128, 32768, int(os.environ.get("S", "256"))
+if CFG == 4:
+    B, n, S = 1, 524288 // R, int(os.environ.get("S", "1024"))
 trace = torch.zeros(B * H * 16, dtype=torch.int64, device="cuda")
 os.environ["SANTA_SAMPLE_TRACE"] = hex(trace.data_ptr())
 import paper_2605_01910_b200 as santa  # noqa: E402
@@ -22,6 +25,13 @@ import santa_inputs as si  # noqa: E402
 if CFG == 5:
     inp = si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=5, workload="lognormal", feature_major=True,
                                 device="cuda")
+elif CFG == 4:
+    from paper_2605_01910_b200 import sharding
+    inp = si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=5, device="cuda")
+    be = sharding.CudaBackend()
+    st4 = be.stats(inp.q, inp.K, inp.seqlens, Hkv, S)
+    stats_all = st4.unsqueeze(0).repeat(R, 1, 1, 1).contiguous()
+    off = torch.zeros(1, dtype=torch.int32, device="cuda")
 else:
     inp = si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=5, device="cuda")
 geo = santa.make_geometry(inp.q, Hkv, n)
@@ -30,7 +40,9 @@ out = torch.empty_like(inp.q)
 
 
 def run(i):
-    if CFG == 5:
+    if CFG == 4:
+        be.sample_gather(stats_all, 0, R, off, inp.V, inp.seqlens, S, "stratified", 13, i)
+    elif CFG == 5:
         santa.santa_decode_attention_bernoulli(geo, inp.q, inp.Kt, inp.V, inp.seqlens, 8, 1, 1, S, "stratified", 13,
                                                i, out, None, ws)
     else:
