@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(D) bern_weights_kernel(BernParams p) {
   const int kvh = blockIdx.x, b = blockIdx.y, i = threadIdx.x;
   const size_t unit = (size_t)b * p.Hkv + kvh;
   const T* q = reinterpret_cast<const T*>(p.q) + ((size_t)b * p.H + (size_t)kvh * G) * D;
+  pdl_wait_primary();  // PDL launch: q (and the workspace) only after the preceding kernel completed
   if (i == 0) sCount = 0;
   double qd[G];
 #pragma unroll

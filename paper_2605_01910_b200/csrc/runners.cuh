@@ -25,13 +25,13 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
       auto kern = score_stream_append_kernel<T, D, G, NW, SPW>;
       if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
       const AppendParams ap{a.k_new, a.v_new, a.K_w, a.V_w};
-      if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p, ap) != cudaSuccess)
+      if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, true, tm, p, ap) != cudaSuccess)
         return SANTA_ERR_CUDA;
       return SANTA_OK;
     }
     auto kern = score_stream_kernel<T, D, G, NW, SPW>;
     if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
-    if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tm, p) != cudaSuccess)
+    if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, a.events == nullptr, tm, p) != cudaSuccess)
       return SANTA_ERR_CUDA;
     return SANTA_OK;
     }
@@ -393,7 +393,7 @@ santa_status RunBern<T, D, G>::run(const DecodeArgs& a, const void* Kt, int nB, 
           !force_fma;
   }
   p.wfrag = tma ? at<uint2>(a.ws, a.L.bfrag) : nullptr;
-  if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, false, p) !=
+  if (launch(bern_weights_kernel<T, D, G>, dim3(a.g->n_kv_heads, a.g->batch), dim3(D), 0, a.st, true, p) !=
       cudaSuccess)
     return SANTA_ERR_CUDA;
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {

@@ -476,6 +476,9 @@ __global__ void __launch_bounds__(kFastThreads, kFastThreads == 128 ? 5 : 1) sam
   }
   FAST_TRACE(1);
   pdl_wait_primary();
+  // the next kernel in the stream (the next layer's score pass, itself waiting on this grid) may
+  // launch now: its set-up overlaps this chain (all CTAs of this one-wave grid are resident)
+  pdl_launch_dependents();
   fast_body<T, D, G>(p, sm, CS, rank, T0);
 }
 

@@ -467,6 +467,7 @@ __device__ float* sample_item(const SampleParams& p, int b, int h, int rank, int
   }
   SANTA_TRACE(1);
   pdl_wait_primary();
+  pdl_launch_dependents();  // the next kernel (waiting on this grid itself) may set up meanwhile
   SANTA_TRACE(2);
 
   const int seqlen = __ldg(p.seqlens + b);

@@ -306,8 +306,12 @@ __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const
       mbar_init(&empty[i], 1);
     }
     fence_mbar_init();
-    if (blockIdx.x == 0 && p.flags) *p.flags = 0u;
   }
+  // launched with programmatic stream serialization: nothing global is read or written before the
+  // preceding kernel has completed (it may have produced q, appended K / V, or still read the
+  // workspace); the launch itself and the barrier set-up overlap its tail
+  pdl_wait_primary();
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p.flags) *p.flags = 0u;
   __syncthreads();
 #ifdef SANTA_SCORE_EARLY_TRIGGER
   pdl_launch_dependents();
