@@ -148,9 +148,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       mbar_init(&empty[i], 1);
     }
     fence_mbar_init();
-    if (blockIdx.x == 0 && p.flags) *p.flags = 0u;
   }
   for (int i = threadIdx.x; i < NW * 8 * kPRow; i += blockDim.x) sPall[i] = 0;
+  pdl_wait_primary();  // PDL launch: global memory only after the preceding kernel completed
+  if (threadIdx.x == 0 && blockIdx.x == 0 && p.flags) *p.flags = 0u;
   __syncthreads();
   pdl_launch_dependents();
   // this CTA's contiguous stage range
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(kDenseCombineThreads) dense_split_combine(Dens
   static_assert(kDQ <= D && D % kDQ == 0, "combine slice");
   __shared__ float sM[NTH], sNum[NTH], sDen[NTH];
   pdl_wait_primary();
+  pdl_launch_dependents();  // the next kernel (waiting on this grid itself) may set up meanwhile
   constexpr int NSL = D / kDQ;
   const int h = blockIdx.x / NSL, dsl = blockIdx.x - h * NSL, b = blockIdx.y, tid = threadIdx.x;
   const int kvh = h / G, gh = h - kvh * G;

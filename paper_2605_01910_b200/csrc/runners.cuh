@@ -287,7 +287,7 @@ santa_status run_dense_split(const DecodeArgs& a, const DenseParams& p) {
   dp.out = a.out;
   dp.flags = p.flags;
   const int grid = std::min(num_sms(), kDenseSplitMaxCtas);
-  if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, false, tk, tv, dp) != cudaSuccess)
+  if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, true, tk, tv, dp) != cudaSuccess)
     return SANTA_ERR_CUDA;
   // slots per head ~ (CTAs per unit + 1) x NW: 16 parts per output coordinate when that is large
   // (config 2: ~19 CTAs per unit -> one L2 round trip), else one 4-part CTA per head (config 3)
