@@ -148,10 +148,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       mbar_init(&empty[i], 1);
     }
     fence_mbar_init();
+    pdl_wait_primary();  // PDL launch: global memory only after the preceding kernel completed (thread 0
+    if (blockIdx.x == 0 && p.flags) *p.flags = 0u;  // waits, the barrier holds the rest: see score_kernels.cuh)
   }
   for (int i = threadIdx.x; i < NW * 8 * kPRow; i += blockDim.x) sPall[i] = 0;
-  pdl_wait_primary();  // PDL launch: global memory only after the preceding kernel completed
-  if (threadIdx.x == 0 && blockIdx.x == 0 && p.flags) *p.flags = 0u;
   __syncthreads();
   pdl_launch_dependents();
   // this CTA's contiguous stage range

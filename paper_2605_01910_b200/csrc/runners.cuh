@@ -31,7 +31,9 @@ santa_status RunScore<T, D, G>::run(const DecodeArgs& a) {
     }
     auto kern = score_stream_kernel<T, D, G, NW, SPW>;
     if (ensure_smem(kern, smem) != cudaSuccess) return SANTA_ERR_CUDA;
-    if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, a.events == nullptr, tm, p) != cudaSuccess)
+    static const bool no_pdl = std::getenv("SANTA_SCORE_NO_PDL") != nullptr;  // A/B switch (tools)
+    if (launch(kern, dim3(grid), dim3(32 * (NW + 1)), smem, a.st, a.events == nullptr && !no_pdl, tm, p) !=
+        cudaSuccess)
       return SANTA_ERR_CUDA;
     return SANTA_OK;
     }

@@ -254,6 +254,14 @@ __device__ __forceinline__ void store_tile_scores(float* sS, int L, int key0, in
 #define SANTA_STREAM_NW 5
 #define SANTA_STREAM_SPW 2
 #endif
+// PDL prologue (profiles/r02/v73_score_prologue_ab.txt): thread 0 executes griddepcontrol.wait after the
+// barrier set-up and zeroes the flag word, the CTA barrier holds every other thread until then (the
+// wait makes the preceding grids' writes visible to the whole grid).  Config 2 pass 14.6 -> 13.05 us,
+// step 22.6 -> 20.7 us; config 3 pass 341 -> 337 us.  Every thread waiting instead (2) cost the
+// config-3 pass 10 % (373 us); 0 = the pre-PDL prologue (tools only, launch without PDL).
+#ifndef SANTA_SCORE_PROLOGUE
+#define SANTA_SCORE_PROLOGUE 1
+#endif
 #ifndef SANTA_STREAM_CTAS
 #define SANTA_STREAM_CTAS 1  // persistent CTAs per SM
 #endif
@@ -306,12 +314,20 @@ __device__ __forceinline__ void score_stream_body(const CUtensorMap* tmKp, const
       mbar_init(&empty[i], 1);
     }
     fence_mbar_init();
+#if SANTA_SCORE_PROLOGUE == 1
+    pdl_wait_primary();
+#endif
+#if SANTA_SCORE_PROLOGUE != 2
+    if (blockIdx.x == 0 && p.flags) *p.flags = 0u;
+#endif
   }
+#if SANTA_SCORE_PROLOGUE == 2
   // launched with programmatic stream serialization: nothing global is read or written before the
   // preceding kernel has completed (it may have produced q, appended K / V, or still read the
   // workspace); the launch itself and the barrier set-up overlap its tail
   pdl_wait_primary();
   if (threadIdx.x == 0 && blockIdx.x == 0 && p.flags) *p.flags = 0u;
+#endif
   __syncthreads();
 #ifdef SANTA_SCORE_EARLY_TRIGGER
   pdl_launch_dependents();

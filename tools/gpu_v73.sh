@@ -1,0 +1,8 @@
+#!/bin/bash
+O=gpurun_out/${1:-r02_v73}; mkdir -p $O
+for B in 1 32; do
+  echo -n "B$B pro1-pdl " >> $O/ab.txt; B=$B timeout 200 python tools/score_prof.py >> $O/ab.txt 2>&1
+  echo -n "B$B pro0-nopdl " >> $O/ab.txt; SANTA_SCORE_NO_PDL=1 SANTA_LIB_PATH=$PWD/gpurun_in/pro0/libsanta.so B=$B timeout 200 python tools/score_prof.py >> $O/ab.txt 2>&1
+  echo -n "B$B pro2-pdl " >> $O/ab.txt; SANTA_LIB_PATH=$PWD/gpurun_in/pro2/libsanta.so B=$B timeout 200 python tools/score_prof.py >> $O/ab.txt 2>&1
+done
+cat $O/ab.txt
