@@ -78,6 +78,7 @@ __global__ void shard_combine_kernel(const float2* __restrict__ cstats, const in
 
 __global__ void append_kv_kernel(void* K, void* V, const void* kn, const void* vn, KvLayout kv,
                                  const int32_t* seqlens, int D, int eb) {
+  pdl_launch_dependents();  // the PDL-launched score pass sets up meanwhile (it waits for this grid)
   const int kvh = blockIdx.x, b = blockIdx.y;
   const int t = __ldg(seqlens + b) - 1;
   if (t < 0) return;
@@ -95,6 +96,7 @@ __global__ void append_kv_kernel(void* K, void* V, const void* kn, const void* v
 // seqlens[b] - 1 -- the H2D copy and the append in one launch.
 __global__ void stage_append_kernel(const uint4* __restrict__ qkv_h, uint4* __restrict__ q_dev, void* K, void* V,
                                     KvLayout kv, const int32_t* seqlens, int D, int eb, int G, int H) {
+  pdl_launch_dependents();  // the PDL-launched score pass sets up during the PCIe reads below
   const int kvh = blockIdx.x, b = blockIdx.y, Hkv = kv.n_kv_heads;
   const int row16 = D * eb / 16;                                 // 16-B words per row
   const size_t q16 = (size_t)gridDim.y * H * row16, k16 = (size_t)gridDim.y * Hkv * row16;

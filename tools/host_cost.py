@@ -22,3 +22,12 @@ measure("binding_score_phase", lambda i: santa.santa_score_phase(geo, inp.q, inp
 launch = santa.prepare_decode(geo, inp.q, inp.K, inp.V, inp.seqlens, 256, "stratified", 7, out, None, ws, stream=st)
 measure("prepared_decode", launch)
 print(json.dumps(res))
+# the host-buffer step (bench's e2e): pinned [q|k_new|v_new] in, pinned out back
+B, H, Hkv, d = 1, 32, 8, 128
+qkvh = torch.randn(B * H * d + 2 * B * Hkv * d).to(torch.bfloat16).pin_memory()
+qkvd = torch.empty_like(qkvh, device="cuda")
+outh = torch.empty(B * H * d, dtype=torch.bfloat16).pin_memory()
+measure("host_packed_step", lambda i: santa.santa_decode_step_host_packed(geo, qkvh, qkvd, inp.K, inp.V, inp.seqlens,
+                                                                          256, "stratified", 7, i, out, outh, ws,
+                                                                          synchronize=False, stream=st))
+print(json.dumps(res))
