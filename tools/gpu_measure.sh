@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 end-of-work measurement: tests, smoke, bench (ours + reference arm), ncu launch list and
 # --set full captures of the two kernels of the AUTO config-2 step.  Output under gpurun_out/$1.
-O=gpurun_out/${1:-r02_final}; mkdir -p $O
+O=gpurun_out/${1:-measure}; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active --format=csv > $O/gpu.txt
 timeout 1500 python -m pytest tests -m gpu -q -rf > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
