@@ -938,8 +938,10 @@ def main():
                       "h2d_bytes_per_step": qkvh.numel() * 2, "d2h_bytes_per_step": outh.numel() * 2,
                       "path": "santa_decode_step_host_packed with pinned host buffers: per step the staging kernel "
                               "reads [q|k_new|v_new] from pinned host memory (zero copy) and appends the KV rows, "
-                              "decode, the sampler writes out into pinned host memory; back-to-back steps, CUDA "
-                              "events"}
+                              "decode, the sampler writes out into pinned host memory; back-to-back asynchronous "
+                              "steps, CUDA events (the staging kernel's PCIe reads are PDL-overlapped with the "
+                              "previous step's sampler; a loop that syncs between steps measures "
+                              "sync_call_latency_us)"}
         # the synchronous single-call latency of the same API (host wall clock incl. the stream sync)
         et = []
         for i in range(args.warmup + args.steps):

@@ -325,7 +325,10 @@ santa_status santa_decode_step_host(const santa_geometry* geo, const void* q_hos
  * written by the decode kernels themselves (out_dev then unused) -- no copy-engine transfers;
  * pageable buffers use cudaMemcpyAsync.  All argument checks run before the first copy or launch
  * (an invalid call leaves the cache untouched).  The host must not modify qkv_host / read out_host
- * before the stream reaches the end of this call's work.
+ * before the stream reaches the end of this call's work.  A page-locked qkv_host must hold the step's
+ * inputs when the call is made: the staging kernel is launched with programmatic dependent launch and
+ * reads it BEFORE the preceding kernel in the stream has finished (its device writes -- q staging, the
+ * cache slot -- wait for that kernel), so it must not be produced by GPU work still in flight.
  * Bytes moved per call: H2D (B*H + 2*B*H_kv)*d*e, D2H B*H*d*e. */
 santa_status santa_decode_step_host_packed(const santa_geometry* geo, const void* qkv_host, void* qkv_dev,
                                            void* K, void* V, const int32_t* seqlens, int32_t S,

@@ -94,21 +94,36 @@ __global__ void append_kv_kernel(void* K, void* V, const void* kn, const void* v
 // its new K/V rows straight from the PINNED host buffer (a device-addressable alias under UVA) with
 // 16-B loads, writes the q rows to the device staging buffer and the K/V rows into the cache slot
 // seqlens[b] - 1 -- the H2D copy and the append in one launch.
-__global__ void stage_append_kernel(const uint4* __restrict__ qkv_h, uint4* __restrict__ q_dev, void* K, void* V,
-                                    KvLayout kv, const int32_t* seqlens, int D, int eb, int G, int H) {
-  pdl_launch_dependents();  // the PDL-launched score pass sets up during the PCIe reads below
+__global__ void __launch_bounds__(128) stage_append_kernel(const uint4* __restrict__ qkv_h, uint4* __restrict__ q_dev,
+                                                          void* K, void* V, KvLayout kv, const int32_t* seqlens, int D,
+                                                          int eb, int G, int H) {
   const int kvh = blockIdx.x, b = blockIdx.y, Hkv = kv.n_kv_heads;
-  const int row16 = D * eb / 16;                                 // 16-B words per row
+  const int row16 = D * eb / 16;                                 // 16-B words per row (<= 32)
   const size_t q16 = (size_t)gridDim.y * H * row16, k16 = (size_t)gridDim.y * Hkv * row16;
   const size_t qsrc = ((size_t)b * H + (size_t)kvh * G) * row16;
-  for (int i = threadIdx.x; i < G * row16; i += blockDim.x) q_dev[qsrc + i] = qkv_h[qsrc + i];
+  const size_t ksrc = q16 + ((size_t)b * Hkv + kvh) * row16;
+  // the PCIe reads first (launched with PDL: they overlap the preceding kernel's tail) ...
+  const int nq = G * row16;                                      // <= 256 = 2 per thread
+  uint4 qv[2], kr = make_uint4(0u, 0u, 0u, 0u), vr = kr;
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (threadIdx.x + 128 * r < nq) qv[r] = qkv_h[qsrc + threadIdx.x + 128 * r];
+  if (threadIdx.x < row16) {
+    kr = qkv_h[ksrc + threadIdx.x];
+    vr = qkv_h[ksrc + k16 + threadIdx.x];
+  }
+  // ... every device write (q staging, cache slot) only after it has completed
+  pdl_wait_primary();
+  pdl_launch_dependents();  // the PDL-launched score pass sets up meanwhile (it waits for this grid)
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+    if (threadIdx.x + 128 * r < nq) q_dev[qsrc + threadIdx.x + 128 * r] = qv[r];
   const int t = __ldg(seqlens + b) - 1;
   if (t < 0) return;
   const int64_t dst16 = kv.row(b, kvh, t, D) * eb / 16;
-  const size_t ksrc = q16 + ((size_t)b * Hkv + kvh) * row16;
-  for (int i = threadIdx.x; i < row16; i += blockDim.x) {
-    reinterpret_cast<uint4*>(K)[dst16 + i] = qkv_h[ksrc + i];
-    reinterpret_cast<uint4*>(V)[dst16 + i] = qkv_h[ksrc + k16 + i];
+  if (threadIdx.x < row16) {
+    reinterpret_cast<uint4*>(K)[dst16 + threadIdx.x] = kr;
+    reinterpret_cast<uint4*>(V)[dst16 + threadIdx.x] = vr;
   }
 }
 
@@ -545,9 +560,10 @@ santa_status santa_decode_step_host_packed(const santa_geometry* g, const void* 
   cudaStream_t st = a.st;
   char* dev = reinterpret_cast<char*>(qkv_dev);
   if (qkv_alias) {
-    stage_append_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(
-        reinterpret_cast<const uint4*>(qkv_alias), reinterpret_cast<uint4*>(dev), K, V, kv_layout(g), seqlens, (int)D,
-        (int)eb, g->n_heads / g->n_kv_heads, g->n_heads);
+    if (launch(stage_append_kernel, dim3(g->n_kv_heads, g->batch), dim3(128), 0, st, true,
+               reinterpret_cast<const uint4*>(qkv_alias), reinterpret_cast<uint4*>(dev), K, V, kv_layout(g), seqlens,
+               (int)D, (int)eb, g->n_heads / g->n_kv_heads, g->n_heads) != cudaSuccess)
+      return SANTA_ERR_CUDA;
   } else {
     if (cudaMemcpyAsync(dev, qkv_host, qb + 2 * kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SANTA_ERR_CUDA;
     append_kv_kernel<<<dim3(g->n_kv_heads, g->batch), 128, 0, st>>>(K, V, dev + qb, dev + qb + kb, kv_layout(g),
