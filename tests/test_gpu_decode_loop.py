@@ -144,3 +144,38 @@ def test_append_dtype_shape_variants(dtype, d, H, Hkv):
     torch.cuda.synchronize()
     assert torch.equal(K, K_ref) and torch.equal(V, V_ref)
     assert torch.equal(idx, idx_ref) and torch.equal(out, out_ref)
+
+
+def test_pdl_chained_steps_see_the_preceding_kernels_writes():
+    """PDL (the score pass, the dense kernel and the Bernoulli weights kernel are launched with
+    programmatic stream serialization and wait in one thread after their barrier set-up): a torch
+    kernel that writes q, K and V immediately before each call, with no sync, must be seen by that
+    call -- 12 back-to-back steps on changing inputs equal the same steps run one at a time with a
+    device sync before each."""
+    B, H, Hkv, d, n, S = 1, 32, 8, 128, [8192], 256
+    base = to_cuda(si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=81))
+    geo = santa.make_geometry(base.q, Hkv, n[0])
+    ws = santa.workspace(geo, S)
+    q, K, V = base.q.clone(), base.K.clone(), base.V.clone()
+    g = torch.Generator(device="cuda").manual_seed(82)
+    qs = [torch.randn(q.shape, generator=g, device="cuda").to(q.dtype) for _ in range(12)]
+    ks = [torch.randn(K.shape[:-2] + (64, d), generator=g, device="cuda").to(K.dtype) for _ in range(12)]
+
+    def run(i, out, sync):
+        if sync:
+            torch.cuda.synchronize()
+        q.copy_(qs[i])                      # producer kernels right before the call
+        K[:, :, :64].copy_(ks[i])
+        V[:, :, 64:128].copy_(ks[i])
+        santa.santa_decode_attention(geo, q, K, V, base.seqlens, S, "stratified", 9, i, out, None, ws)
+        d_out = out.clone()
+        santa.santa_dense_reference(geo, q, K, V, base.seqlens, out, ws)
+        return d_out, out.clone()
+
+    outs = [torch.empty_like(q) for _ in range(12)]
+    fast = [run(i, outs[i], False) for i in range(12)]
+    ref = [run(i, outs[i], True) for i in range(12)]
+    torch.cuda.synchronize()
+    for i in range(12):
+        assert torch.equal(fast[i][0], ref[i][0]), i
+        assert torch.equal(fast[i][1], ref[i][1]), i
