@@ -261,7 +261,7 @@ const char* santa_status_string(santa_status s) {
 }
 
 const char* santa_version(void) {
-  return "libsanta 0.3 sm_100a (santa_step_kernel: single-launch persistent step, tagged-word publication; santa_step_tc_kernel: tcgen05 score stage, TMEM accumulators; score_stream: TMA 128B-swizzle ring + mma.sync, interleaved; sample_gather: thread-block clusters; prop/flash: S^2ANTA-prop and -flash tile estimators; dense: TMA flash-decoding; bernoulli)";
+  return "libsanta 0.4 sm_100a (santa_step_kernel: single-launch persistent step, tagged-word publication; santa_step_tc_kernel: tcgen05 score stage, TMEM accumulators; score_stream: TMA 128B-swizzle ring + mma.sync, interleaved, PDL-chained; sample_fast / sample_gather: thread-block clusters, 4-per-SM build for large batches; prop/flash: S^2ANTA-prop and -flash tile estimators; dense: TMA flash-decoding; bernoulli: bulk-copy ring + mma.sync with a 3-way bf16 weight split; peer_exchange: one-shot P2P collectives)";
 }
 
 int32_t santa_auto_path(const santa_geometry* g, int32_t S) {
