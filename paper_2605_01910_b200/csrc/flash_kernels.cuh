@@ -53,6 +53,7 @@ __device__ float* flash_item(const SampleParams& p, int b, int h, int rank, int 
   __shared__ float sred_f[32];
 
   pdl_wait_primary();
+  pdl_launch_dependents();  // the next step's PDL-launched score pass may set up meanwhile
   const int seqlen = __ldg(p.seqlens + b);
   const int nC = seqlen > 0 ? (seqlen + p.L - 1) / p.L : 0;
   const int Tt = (nC + CPT - 1) / CPT;

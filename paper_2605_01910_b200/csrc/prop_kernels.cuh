@@ -55,6 +55,7 @@ __device__ float* prop_item(const SampleParams& p, int b, int h, int rank, int C
   __shared__ unsigned long long sCand[32];
 
   pdl_wait_primary();
+  pdl_launch_dependents();  // the next step's PDL-launched score pass may set up meanwhile
   const int seqlen = __ldg(p.seqlens + b);
   if (seqlen < 1) {  // empty distribution: zero output, flag, no sampling
     for (int d = tid; d < D; d += NT) sPart[d] = 0.f;

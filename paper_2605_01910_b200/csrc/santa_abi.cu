@@ -46,6 +46,7 @@ int flash_max_samples(const santa_geometry* g, int S, int tile_len, int* cpt_out
 __global__ void shard_combine_kernel(const float2* __restrict__ cstats, const int32_t* __restrict__ seqlens,
                                      int H, int Cmax, int L, double* __restrict__ stats_out) {
   pdl_wait_primary();
+  pdl_launch_dependents();  // a following PDL-launched score pass may set up meanwhile
   const int h = blockIdx.x, b = blockIdx.y;
   const int seqlen = __ldg(seqlens + b);
   const int nC = seqlen > 0 ? (seqlen + L - 1) / L : 0;
