@@ -782,7 +782,10 @@ def main():
                                "kernel": "score_stream_kernel<bf16,128,4,5,2> (split-KV score pass, interleaved)",
                                "peak_source": peak_src, "algorithmic_bytes_per_launch": kb + B * H * d * 2,
                                "kernel_us": round(sms * 1e3, 2),
-                               "timing": "the pass alone, back-to-back over rotating KV caches > 4x L2, CUDA events",
+                               "timing": ("the pass alone, back-to-back over rotating KV caches > 4x L2, CUDA events; "
+                                          "launches PDL-chained (each waits for its predecessor before touching memory, "
+                                          "its launch and set-up overlap the predecessor's tail; a serialised cold "
+                                          "launch under ncu is ~17 us)"),
                                "sample_phase_us": round(sgms * 1e3, 2), "share_of_step": round(sms / ms, 3)}
         else:
             achieved = bytes_step / (ms * 1e-3) / 1e9
