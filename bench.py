@@ -696,6 +696,18 @@ def main():
             dist.barrier()
         return e0.elapsed_time(e1) / K
 
+    def local_loop(fn, K):
+        """timed_loop without the cross-rank barriers: for legs one rank runs alone (rank 0's library
+        baselines), where a barrier would pair with another rank's unrelated collective."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(K):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / K
+
     def max_over_ranks(x):
         if world == 1:
             return x
@@ -973,7 +985,7 @@ def main():
                               if args.dist_backend == "nccl" else None,
                               "nccl_debug": os.environ.get("NCCL_DEBUG")}
     if not args.no_extras and not args.no_baselines and rank == 0 and args.batch == 1 and not args.page_size:
-        res["library_baselines"] = library_baselines(probs, NR, timed_loop, args)
+        res["library_baselines"] = library_baselines(probs, NR, local_loop, args)
         d = res["library_baselines"]
         for k in ("flashinfer_decode_us", "flash_attn_2_decode_us", "torch_sdpa_us"):
             if isinstance(d.get(k), float):
