@@ -356,3 +356,26 @@ def test_dense_reference_split_shapes(B, n, units):
                              si.as_bits(inp.V[b:b + 1, kvh:kvh + 1]), lens[b:b + 1])
         err = np.abs(out[b:b + 1, hs].float().cpu().numpy() - ref).max()
         assert err <= 2e-2, (b, kvh, err)
+
+
+@pytest.mark.parametrize("paged", [False, True])
+def test_large_batch_sampler_paged_and_ragged(paged):
+    """The 4-CTA-per-SM sampler build (more than two sampler CTAs per SM: 12 x 32 = 384 heads) on a
+    ragged batch, contiguous and through a 64-key page table: the same indices and outputs as the
+    single-launch step kernel (independent sampler code), and oracle parity on sampled units incl. the
+    shortest sequence."""
+    n = [4096, 1500, 33, 4095, 64, 2047, 3000, 129, 4000, 1, 2500, 4096]
+    inp = to_cuda(si.make_decode_inputs(12, 32, 8, 128, n, dtype="bf16", seed=91, workload="temp4",
+                                        page_size=64 if paged else 0))
+    S = 128
+    out, idx = gpu_decode(inp, S, "stratified", seed=5, offset=2, paged=paged, path="two_kernel")
+    out2, idx2 = gpu_decode(inp, S, "stratified", seed=5, offset=2, paged=paged, path="step")
+    assert (idx != idx2).float().mean().item() < 2e-3
+    G = 4
+    for b, kvh in [(2, 0), (9, 3), (11, 7)]:
+        sub = si.DecodeInputs(q=inp.q[b:b + 1, G * kvh:G * (kvh + 1)].contiguous(),
+                              K=inp.K[b:b + 1, kvh:kvh + 1].contiguous(), V=inp.V[b:b + 1, kvh:kvh + 1].contiguous(),
+                              seqlens=inp.seqlens[b:b + 1].contiguous(), n_heads=G, n_kv_heads=1, head_dim=128,
+                              dtype="bf16")
+        check_parity(sub, out[b:b + 1, G * kvh:G * (kvh + 1)], idx[b:b + 1, G * kvh:G * (kvh + 1)], S, "stratified",
+                     5, 2, head_offset=G * kvh, batch_offset=b)
