@@ -379,3 +379,41 @@ def test_large_batch_sampler_paged_and_ragged(paged):
                               dtype="bf16")
         check_parity(sub, out[b:b + 1, G * kvh:G * (kvh + 1)], idx[b:b + 1, G * kvh:G * (kvh + 1)], S, "stratified",
                      5, 2, head_offset=G * kvh, batch_offset=b)
+
+
+def test_seqshard_large_batch_sampler():
+    """Sequence sharding with more sampler CTAs than two per SM (12 x 32 heads: the 4-per-SM build in
+    phase 2, strata of other shards skipped): two simulated shards' merged indices equal the unsharded
+    run and every stratum is owned by exactly one shard."""
+    from paper_2605_01910_b200 import sharding
+    n = [6000, 3001, 4096, 129, 5000, 6000, 2048, 777, 6000, 4500, 1000, 6000]
+    B, H, Hkv, d, S = 12, 32, 8, 128, 256
+    inp = to_cuda(si.make_decode_inputs(B, H, Hkv, d, n, dtype="bf16", seed=93))
+    full_out, full_idx = gpu_decode(inp, S, "stratified", seed=8, offset=1)
+    R = 2
+    parts, owner = [], torch.zeros(B, H, S, dtype=torch.int32, device="cuda")
+    merged = torch.full((B, H, S), -1, dtype=torch.int32, device="cuda")
+    stats, shards = [], []
+    for r in range(R):
+        lo, ln = sharding.shard_ranges(inp.seqlens, r, R, "cuda")
+        nloc = int(ln.max())
+        Ks = torch.zeros(B, Hkv, nloc, d, dtype=inp.K.dtype, device="cuda")
+        Vs = torch.zeros_like(Ks)
+        for b in range(B):
+            a, e = int(lo[b]), int(lo[b]) + int(ln[b])
+            Ks[b, :, :e - a] = inp.K[b, :, a:e]
+            Vs[b, :, :e - a] = inp.V[b, :, a:e]
+        be = sharding.CudaBackend()
+        stats.append(be.stats(inp.q, Ks, ln, Hkv, S))
+        shards.append((be, Vs, ln, lo))
+    stats_all = torch.stack(stats, 0)
+    total = torch.zeros(B, H, d, dtype=torch.float32, device="cuda")
+    for r, (be, Vs, ln, lo) in enumerate(shards):
+        part, idx = be.sample_gather(stats_all, r, R, lo, Vs, ln, S, "stratified", 8, 1, return_idx=True)
+        total += part
+        owner += (idx >= 0).int()
+        merged = torch.where(idx >= 0, idx, merged)
+    torch.cuda.synchronize()
+    assert torch.all(owner == 1)
+    assert (merged != full_idx).float().mean().item() < 2e-3
+    assert (total.to(torch.bfloat16).float() - full_out.float()).abs().max().item() < 3e-2
