@@ -551,19 +551,26 @@ def config4_seqshard(args, dev, stream, timed_loop, max_over_ranks, peak, world,
                     "whole 512k sequence")}
     if not args.share_gpu:
         # the same step with both exchanges as one-shot peer-memory kernels (CUDA-IPC mapped buffers,
-        # NVLink P2P stores + flags); never with ranks sharing one GPU (they would wait on each other)
-        ex = sharding.PeerExchange(1 * H * d * 4, device=dev)
-
-        def full_peer(i):
-            sharding.seqshard_decode(q, loc.K, loc.V, seqlens, S, args.mode, args.seed, i, backend=be, ranges=ranges,
-                                     exchange=ex)
-        for i in range(3):
-            full_peer(i)
-        tp = max_over_ranks(timed_loop(full_peer, steps))
-        out["peer_exchange"] = {"us": round(tp * 1e3, 2), "GBps": round(kb / (tp * 1e-3) / 1e9, 1),
-                                "collectives_us": round(max(0.0, tp - t1 - t2) * 1e3, 2),
-                                "note": "santa_peer_allgather + santa_peer_allreduce_f32 instead of NCCL"}
-        ex.close()
+        # NVLink P2P stores + flags); never with ranks sharing one GPU (they would wait on each other).
+        # Every rank must agree on whether the mapping worked before any rank launches a peer kernel.
+        ex, err = None, ""
+        try:  # all ranks raise together if any rank cannot map the buffers (PeerExchange)
+            ex = sharding.PeerExchange(1 * H * d * 4, device=dev)
+        except Exception as e:  # e.g. no P2P / IPC between the GPUs of this node
+            err = repr(e)[:200]
+        if ex is not None:
+            def full_peer(i):
+                sharding.seqshard_decode(q, loc.K, loc.V, seqlens, S, args.mode, args.seed, i, backend=be,
+                                         ranges=ranges, exchange=ex)
+            for i in range(3):
+                full_peer(i)
+            tp = max_over_ranks(timed_loop(full_peer, steps))
+            out["peer_exchange"] = {"us": round(tp * 1e3, 2), "GBps": round(kb / (tp * 1e-3) / 1e9, 1),
+                                    "collectives_us": round(max(0.0, tp - t1 - t2) * 1e3, 2),
+                                    "note": "santa_peer_allgather + santa_peer_allreduce_f32 instead of NCCL"}
+            ex.close()
+        else:
+            out["peer_exchange"] = {"unavailable": err}
     del loc, be
     torch.cuda.empty_cache()
     return out

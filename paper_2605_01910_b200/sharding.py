@@ -152,19 +152,37 @@ class PeerExchange:
         self.max_payload = max_payload_bytes
         self.buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device)
         torch.cuda.synchronize(self.buf.device)
+        # every rank takes part in every collective below whatever fails locally, and all ranks raise
+        # together if any rank could not export / map (no rank is left waiting in a collective)
+        err = None
+        try:
+            mine = santa_ipc_export(self.buf)
+        except Exception as e:  # noqa: BLE001
+            mine, err = None, e
         handles = [None] * self.world
-        dist.all_gather_object(handles, santa_ipc_export(self.buf), group=group)
+        dist.all_gather_object(handles, mine, group=group)
         self._bases, ptrs = [], []
-        for r, (h, off) in enumerate(handles):
-            if r == self.rank:
-                ptrs.append(self.buf.data_ptr())
-            else:
-                p, base = santa_ipc_import(h, off)
-                ptrs.append(p)
-                self._bases.append(base)
+        if err is None and all(h is not None for h in handles):
+            try:
+                for r, (h, off) in enumerate(handles):
+                    if r == self.rank:
+                        ptrs.append(self.buf.data_ptr())
+                    else:
+                        p, base = santa_ipc_import(h, off)
+                        ptrs.append(p)
+                        self._bases.append(base)
+            except Exception as e:  # noqa: BLE001
+                err = e
+        ok = torch.tensor([1.0 if err is None and len(ptrs) == self.world else 0.0], device=self.buf.device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if ok.item() != 1.0:
+            from . import santa_ipc_close
+            for b in self._bases:
+                santa_ipc_close(b)
+            self._bases = []
+            raise RuntimeError(f"PeerExchange: exchange buffers could not be mapped on every rank ({err!r})")
         self.peer_group = make_peer_group(ptrs, self.nbytes)
         self.epoch = 0
-        dist.barrier(group=group)
 
     def all_gather(self, t: torch.Tensor) -> torch.Tensor:
         from . import santa_peer_allgather

@@ -202,3 +202,48 @@ def test_ipc_mapping_two_processes():
     for _ in range(2):
         r = q.get(timeout=5)
         assert r == "ok", r
+
+
+def _peer_exchange_worker(rank, world, port, q):
+    """sharding.PeerExchange built by two processes on one GPU (export, all_gather_object of the
+    handles, import, the all-ranks success vote): every rank sees both buffers; rank 0 then pushes one
+    emulated all-gather through rank 1's mapping (no kernel waits on another process) and rank 1 finds
+    the flags in its own buffer; close() unmaps."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2605_01910_b200 as sa
+        from paper_2605_01910_b200 import sharding as sh
+        ex = sh.PeerExchange(1024, device="cuda")
+        assert ex.world == 2 and ex.peer_group.world == 2
+        assert ex.peer_group.bufs[rank] == ex.buf.data_ptr()
+        if rank == 0:
+            src = [torch.full((256,), float(r + 1), device="cuda") for r in range(2)]
+            dst = [torch.empty(2 * 256, device="cuda") for _ in range(2)]
+            sa.santa_peer_allgather(ex.peer_group, [0, 1], src, dst, 1)
+            torch.cuda.synchronize()
+            assert torch.equal(dst[1][:256], src[0]) and torch.equal(dst[1][256:], src[1])
+        dist.barrier()
+        if rank == 1:
+            flags = ex.buf[256:256 + 4096].view(torch.int32).view(2, 8, 64)
+            assert int(flags[1, 0, 0]) == 1 and int(flags[1, 1, 0]) == 1
+        ex.close()
+        q.put("ok")
+    except Exception as e:
+        q.put(repr(e))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_class_two_processes():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    mp.start_processes(_peer_exchange_worker, args=(2, _free_port(), q), nprocs=2, join=True, start_method="spawn")
+    for _ in range(2):
+        r = q.get(timeout=5)
+        assert r == "ok", r
