@@ -170,15 +170,12 @@ santa_status validate_bern(const santa_geometry* g, const void* q, const void* K
 }
 
 int auto_path(const santa_geometry* g, int S) {
-  const bool step_ok = g->dtype != SANTA_F32 && g->max_seqlen <= 65536;
-  const bool tc_pages = !g->page_table || g->page_size % kTcTileKeys == 0;
-  if (step_ok && (int64_t)g->batch * g->n_heads >= kTcMinHeads) {
-    // batch 32 (tools/path_sweep.py, profiles/r02/v49_path_sweep.json): since the 4-CTA-per-SM
-    // sampler the two-kernel path wins from S = 256 (389 vs 396 us for tcgen05 at S = 256, 413 vs 422
-    // us for the mma.sync step kernel at S = 512); at S = 64 the tcgen05 step kernel still samples
-    // under the stream for less (365 vs 369 us)
-    if (S <= 64 && tc_pages) return SANTA_PATH_STEP_TC;
-  }
+  // The score pass + sampler kernel everywhere since the round-2 changes (PDL-chained pass, 4-CTA-per-SM
+  // sampler): config 2 20.1-21.1 vs 25.1-25.9 (step) / 28.9-29.2 us (tcgen05 step); batch 32 360-361 vs
+  // 366 us for the tcgen05 step kernel at S = 64 and 381-386 vs 394 us at S = 256
+  // (profiles/r02/v95_path_sweep_step_pdl.txt, v49_path_sweep.json).  The step kernels stay selectable.
+  (void)g;
+  (void)S;
   return SANTA_PATH_TWO_KERNEL;
 }
 

@@ -103,10 +103,10 @@ def test_product_package_never_imports_the_oracle():
 
 
 def test_auto_path_policy_is_host_logic():
-    """santa_auto_path (pure host arithmetic): the two-kernel path except from 1024 query heads with
-    S <= 64 (the tcgen05 step kernel), measured in profiles/r02/v49_path_sweep.json."""
+    """santa_auto_path (pure host arithmetic): the two-kernel path for every geometry since round 2
+    (profiles/r02/v95_path_sweep_step_pdl.txt)."""
     assert santa.santa_auto_path(_geo(), 256) == "two_kernel"             # config 2
-    assert santa.santa_auto_path(_geo(batch=32), 64) == "step_tc"         # config 3, S = 64
+    assert santa.santa_auto_path(_geo(batch=32), 64) == "two_kernel"      # config 3, S = 64
     assert santa.santa_auto_path(_geo(batch=32), 256) == "two_kernel"     # config 3, S = 256
     assert santa.santa_auto_path(_geo(batch=32), 512) == "two_kernel"
     assert santa.santa_auto_path(_geo(batch=32), 1024) == "two_kernel"

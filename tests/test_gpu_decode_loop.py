@@ -34,7 +34,7 @@ def _new_rows(B, Hkv, d, dtype, seed):
 
 @pytest.mark.parametrize("B,H,n,S,want_path", [(2, 32, [3000, 1501], 128, "two_kernel"),
                                                (1, 32, [4096], 256, "two_kernel"),
-                                               (32, 32, [2048] * 32, 64, "step_tc")])
+                                               (32, 32, [2048] * 32, 64, "two_kernel")])
 def test_append_equals_torch_append_then_decode(B, H, n, S, want_path):
     inp = to_cuda(si.make_decode_inputs(B, H, 8, 128, n, dtype="bf16", seed=71))
     geo = santa.make_geometry(inp.q, 8, inp.K.shape[2])
